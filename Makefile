@@ -1,0 +1,24 @@
+# Builds paper_2209_06916_b200/_lib/libmgrit_b200.so for sm_100a (B200).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v --expt-relaxed-constexpr
+SRC := paper_2209_06916_b200/csrc
+OUT := paper_2209_06916_b200/_lib
+BUILD := build/obj
+OBJS := $(BUILD)/mgb_host.o $(BUILD)/k_win_exact.o $(BUILD)/k_win_fast.o $(BUILD)/k_gen.o $(BUILD)/k_rk.o
+HDRS := $(SRC)/mgb_device.cuh $(SRC)/mgb_registry.h include/mgrit_b200.h
+
+all: $(OUT)/libmgrit_b200.so
+
+$(BUILD)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ > $(BUILD)/$*.ptxas.log 2>&1 || (cat $(BUILD)/$*.ptxas.log; exit 1)
+
+$(OUT)/libmgrit_b200.so: $(OBJS)
+	@mkdir -p $(OUT)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+
+clean:
+	rm -rf build $(OUT)/libmgrit_b200.so
+
+.PHONY: all clean

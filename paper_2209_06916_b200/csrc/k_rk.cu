@@ -1,0 +1,19 @@
+// Staged Runge-Kutta relaxation (explicit or SDIRK with factorised stage solves).
+#include "mgb_registry.h"
+
+namespace mgb {
+#define RK_P(P)                   \
+  MGB_REG(K_RK, P, 0, 1, true); \
+  MGB_REG(K_RK, P, 0, 2, true); \
+  MGB_REG(K_RK, P, 0, 3, true); \
+  MGB_REG(K_RK, P, 0, 4, true); \
+  MGB_REG(K_RK, P, 0, 5, true); \
+  MGB_REG(K_RK, P, 0, 6, true);
+void register_rk() {
+  RK_P(1)
+  RK_P(2)
+  RK_P(4)
+  RK_P(8)
+  RK_P(16)
+}
+}  // namespace mgb

@@ -1,0 +1,689 @@
+// mgb_device.cuh -- device side of the B200 MGRIT hot path (sm_100a).
+//
+// One CTA owns one CF-interval at a time and keeps that interval's periodic
+// FP64 slice resident in shared memory for all of its fine steps (the
+// reference walks the same steps as batched numpy calls, mgrit.py:132-142).
+//
+// Data layout of a resident slice (n = T*P points, T owning threads, P points
+// per thread, P a power of two <= 16):
+//   point i is owned by thread t = i / P as chunk element q = i % P and lives
+//   at shared address q*S + t, with S = T + pad chosen so that (a) every
+//   stencil / window read (fixed q, consecutive t) and (b) the natural-order
+//   row copies to and from HBM are both bank-conflict free.
+// Every thread keeps its own chunk in registers; stencil taps read neighbours
+// from shared memory; periodic wrap-around is an index wrap on t.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/mgrit_b200.h"
+
+namespace mgb {
+
+constexpr int MAXP = 16;
+constexpr int MAX_TAPS = 256;
+constexpr int MAX_TAPS2 = 32;
+constexpr int MAX_FAC = 8;
+constexpr int MAX_ST = 6;
+constexpr int LOGT = 11;
+constexpr int MAX_CAP = 128;
+constexpr int MAX_WIN = 31;  // register-window stencils: span <= 30
+
+enum { K_WIN = 0, K_GEN = 1, K_RK = 2, K_SLD = 3, K_SLG = 4 };
+
+// One periodic first/second-order recurrence factor of a factorised
+// circulant (see bandsolve in mgb_host.cu):
+//   y_i = b_i + a1*y_{i-1} + a2*y_{i-2}   (dir = +1; dir = -1 runs i downward)
+// Tables are precomputed in long double for the launch geometry (T, P).
+struct Factor {
+  double a1, a2;
+  int dir, pad_;
+  double h1[MAXP], h2[MAXP];  // first row of A^(q+1): response to the carry-in state
+  double M[4];                // A^P: chunk transition
+  double Mpow[LOGT][4];       // M^(2^k)
+  double MR[5][4];            // (M^R)^(2^d), R = ceil(T/32): lane scan multipliers
+  double Winv[4];             // (I - M^T)^-1: periodic closure
+};
+
+struct StepParams {
+  int kind, n, P, T, S, exact, repeat, stages;
+  int implicit, nfac, shift, cap;
+  int ntap, ntap2, win_lo, win_span;
+  double gain_inv, tol;
+  double A[MAX_ST * MAX_ST], b[MAX_ST];
+  int tap_off[MAX_TAPS];
+  double tap_w[MAX_TAPS];
+  int tap2_off[MAX_TAPS2];
+  double tap2_w[MAX_TAPS2];
+  double win_w[32];
+  Factor fac[MAX_FAC];
+};
+static_assert(sizeof(StepParams) % 16 == 0, "StepParams must be 16-byte sized");
+
+struct RelaxLaunch {
+  mgb_relax_args a;
+  double* ws;            // GMRES workspace base (slot = blockIdx.x)
+  long long ws_slot;     // doubles per slot
+};
+
+// ---------------------------------------------------------------- helpers
+
+template <bool EXACT>
+__device__ __forceinline__ double madd(double acc, double w, double v) {
+  // EXACT: numpy's `out += w * roll(v)` -- product rounded, then sum rounded.
+  if (EXACT) return __dadd_rn(acc, __dmul_rn(w, v));
+  return fma(w, v, acc);
+}
+
+template <int P>
+__device__ __forceinline__ int saddr(int e, int S) {
+  return (e & (P - 1)) * S + e / P;
+}
+
+template <int P>
+__device__ __forceinline__ void load_chunk(const double* __restrict__ src, int t, double (&x)[P]) {
+  const double* s = src + (size_t)t * P;
+  if constexpr (P % 2 == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(s);
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      double2 v = __ldg(s2 + q);
+      x[2 * q] = v.x;
+      x[2 * q + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] = __ldg(s + q);
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void store_chunk(double* dst, int t, const double (&x)[P]) {
+  double* d = dst + (size_t)t * P;
+  if constexpr (P % 2 == 0) {
+    double2* d2 = reinterpret_cast<double2*>(d);
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) d2[q] = make_double2(x[2 * q], x[2 * q + 1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < P; ++q) d[q] = x[q];
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void chunk_to_row(double* row, int t, int S, const double (&x)[P]) {
+#pragma unroll
+  for (int q = 0; q < P; ++q) row[q * S + t] = x[q];
+}
+
+// natural-order copy of the resident slice to HBM (coalesced, streaming:
+// F-point rows are not re-read before the next cycle overwrites them)
+template <int P>
+__device__ __forceinline__ void row_to_global(const double* row, double* dst, int n, int S) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) __stcs(dst + i, row[saddr<P>(i, S)]);
+}
+
+struct Ctx {
+  const StepParams* sp;
+  double* row;
+  double* red;   // 2 x 32 reduction slots
+  double* bc;    // broadcast scalars
+  double* scan;  // 4*T: recurrence carry states
+  double* gm;    // GMRES: Hessenberg column + y
+  double* ws;    // GMRES: per-CTA global workspace
+  int t, T, S, n;
+  bool own;
+  int parity;
+};
+
+// Deterministic block reduction: warp butterfly, then every thread sums the
+// warp partials in warp order -> bitwise identical result in all threads.
+__device__ __forceinline__ double block_sum(Ctx& c, double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* slot = c.red + (c.parity << 5);
+  if (lane == 0) slot[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += slot[i];
+  c.parity ^= 1;
+  return s;
+}
+
+// ---------------------------------------------------------------- stencils
+
+// generic taps (offsets pre-reduced to [0, n)), read from shared memory
+template <int P, bool EXACT>
+__device__ __forceinline__ void stencil_gen(const Ctx& c, int ntap, const int* off, const double* w,
+                                            double (&y)[P]) {
+#pragma unroll
+  for (int q = 0; q < P; ++q) y[q] = 0.0;
+  if (!c.own) return;
+  for (int k = 0; k < ntap; ++k) {
+    const int o = off[k];
+    const double wk = w[k];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const int cq = o + q;
+      int tt = c.t + cq / P;
+      tt = tt >= c.T ? tt - c.T : tt;
+      y[q] = madd<EXACT>(y[q], wk, c.row[(cq & (P - 1)) * c.S + tt]);
+    }
+  }
+}
+
+// contiguous short stencil: each thread loads a register window of P+SPAN
+// neighbours once and produces P outputs (reuse factor (SPAN+1)P/(P+SPAN)).
+template <int P, int SPAN, bool EXACT>
+__device__ __forceinline__ void stencil_win(const Ctx& c, int tb, int r0, const double (&wd)[SPAN + 1],
+                                            double (&y)[P]) {
+  if (!c.own) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) y[q] = 0.0;
+    return;
+  }
+  double win[P + SPAN];
+#pragma unroll
+  for (int w = 0; w < P + SPAN; ++w) {
+    const int cw = r0 + w;
+    int tt = tb + cw / P;
+    tt = tt >= c.T ? tt - c.T : tt;
+    win[w] = c.row[(cw & (P - 1)) * c.S + tt];
+  }
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k <= SPAN; ++k) acc = madd<EXACT>(acc, wd[k], win[q + k]);
+    y[q] = acc;
+  }
+}
+
+// ------------------------------------------------ factorised periodic solve
+
+__device__ __forceinline__ void mv2(const double* M, double& x1, double& x2) {
+  const double n1 = fma(M[0], x1, M[1] * x2);
+  const double n2 = fma(M[2], x1, M[3] * x2);
+  x1 = n1;
+  x2 = n2;
+}
+
+// warp 0: carry-in states of all logical chunks for one factor.
+__device__ __forceinline__ void lane_scan(const Factor& F, const double* st, double* cin, double* sb,
+                                          int T, int lane) {
+  const int R = (T + 31) >> 5;
+  const int base = lane * R;
+  double X1 = 0.0, X2 = 0.0;
+  for (int i = 0; i < R; ++i) {
+    const int tl = base + i;
+    double b1 = 0.0, b2 = 0.0;
+    if (tl < T) {
+      b1 = st[2 * tl];
+      b2 = st[2 * tl + 1];
+    }
+    mv2(F.M, X1, X2);
+    X1 += b1;
+    X2 += b2;
+  }
+  double Y1 = X1, Y2 = X2;
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    const int off = 1 << d;
+    double p1 = __shfl_up_sync(0xffffffffu, Y1, off);
+    double p2 = __shfl_up_sync(0xffffffffu, Y2, off);
+    if (lane >= off) {
+      mv2(F.MR[d], p1, p2);
+      Y1 += p1;
+      Y2 += p2;
+    }
+  }
+  double s1 = __shfl_up_sync(0xffffffffu, Y1, 1);
+  double s2 = __shfl_up_sync(0xffffffffu, Y2, 1);
+  if (lane == 0) s1 = s2 = 0.0;
+  for (int i = 0; i < R; ++i) {
+    const int tl = base + i;
+    if (tl < T) {
+      cin[2 * tl] = s1;
+      cin[2 * tl + 1] = s2;
+      mv2(F.M, s1, s2);
+      s1 += st[2 * tl];
+      s2 += st[2 * tl + 1];
+      if (tl == T - 1) {  // zero-start end state -> periodic closure
+        double w1 = s1, w2 = s2;
+        mv2(F.Winv, w1, w2);
+        sb[0] = w1;
+        sb[1] = w2;
+      }
+    }
+  }
+}
+
+// x <- A^{-1} x for the factorised circulant A = K S^s prod_f F_f (in registers)
+template <int P>
+__device__ void chain_solve(Ctx& c, double (&x)[P]) {
+  const StepParams& sp = *c.sp;
+  const int T = c.T, t = c.t;
+  double* st = c.scan;
+  double* cin = c.scan + 2 * T;
+  double* sb = c.bc + 4;
+  if (sp.shift != 0) {
+    __syncthreads();
+    if (c.own) chunk_to_row<P>(c.row, t, c.S, x);
+    __syncthreads();
+    if (c.own) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        int e = t * P + q - sp.shift;
+        e %= c.n;
+        e = e < 0 ? e + c.n : e;
+        x[q] = c.row[saddr<P>(e, c.S)];
+      }
+    }
+  }
+  for (int f = 0; f < sp.nfac; ++f) {
+    const Factor& F = sp.fac[f];
+    const bool fwd = F.dir > 0;
+    const int tl = fwd ? t : T - 1 - t;
+    if (c.own) {
+      const double a1 = F.a1, a2 = F.a2;
+      double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < P; ++qq) {
+        const int q = fwd ? qq : P - 1 - qq;
+        const double yv = fma(a2, s2, fma(a1, s1, x[q]));
+        x[q] = yv;
+        s2 = s1;
+        s1 = yv;
+      }
+      st[2 * tl] = s1;
+      st[2 * tl + 1] = s2;
+    }
+    __syncthreads();
+    if (t < 32) lane_scan(F, st, cin, sb, T, t);
+    __syncthreads();
+    if (c.own) {
+      double c1 = cin[2 * tl], c2 = cin[2 * tl + 1];
+      double p1 = sb[0], p2 = sb[1];
+#pragma unroll
+      for (int kb = 0; kb < LOGT; ++kb)
+        if ((tl >> kb) & 1) mv2(F.Mpow[kb], p1, p2);
+      c1 += p1;
+      c2 += p2;
+#pragma unroll
+      for (int qq = 0; qq < P; ++qq) {
+        const int q = fwd ? qq : P - 1 - qq;
+        x[q] = fma(F.h1[qq], c1, fma(F.h2[qq], c2, x[q]));
+      }
+    }
+  }
+  if (c.own) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] *= sp.gain_inv;
+  }
+}
+
+// ------------------------------------------------------------------ GMRES
+
+// Unrestarted GMRES(x0 = 0) on the circulant (taps2) for the CTA's row,
+// following circulant.py:262-332: MGS Arnoldi, Givens QR, stop when
+// res <= tol or ||h|| <= 1e-14 beta, back substitution, x = V y.
+// V lives in this CTA's HBM/L2 workspace slot, element (t, q) at q*T + t.
+template <int P>
+__device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& depth_out,
+                            double& res_out) {
+  const StepParams& sp = *c.sp;
+  const int n = c.n, T = c.T, t = c.t;
+  const int cap = sp.cap;
+  double* V = c.ws;
+  double* R = V + (size_t)(cap + 1) * n;
+  double* cs = R + (size_t)cap * cap;
+  double* sn = cs + cap;
+  double* gg = sn + cap;
+  double* hcol = c.gm;
+  double* ybuf = c.gm + MAX_CAP + 2;
+
+  double part = 0.0;
+  if (c.own) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) part = fma(b[q], b[q], part);
+  }
+  const double beta = sqrt(block_sum(c, part));
+#pragma unroll
+  for (int q = 0; q < P; ++q) x[q] = 0.0;
+  if (beta == 0.0) {  // zero right-hand side: x = 0, converged (circulant.py:274-278)
+    depth_out = 0;
+    res_out = 0.0;
+    return;
+  }
+  double v[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) v[q] = b[q] / beta;
+  if (c.own) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) V[q * T + t] = v[q];
+  }
+  if (t == 0) gg[0] = beta;
+  double res = 1.0;
+  int depth = 0;
+  for (int j = 0; j < cap; ++j) {
+    __syncthreads();
+    if (c.own) chunk_to_row<P>(c.row, t, c.S, v);
+    __syncthreads();
+    double w[P];
+    stencil_gen<P, true>(c, sp.ntap2, sp.tap2_off, sp.tap2_w, w);
+    // modified Gram-Schmidt (next basis vector prefetched from L2)
+    double vn[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) vn[q] = 0.0;
+    if (c.own && j > 0) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) vn[q] = V[q * T + t];
+    }
+    for (int i = 0; i <= j; ++i) {
+      double vi[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) vi[q] = (i == j) ? v[q] : vn[q];
+      if (c.own && i + 1 < j) {
+        const double* Vn = V + (size_t)(i + 1) * n;
+#pragma unroll
+        for (int q = 0; q < P; ++q) vn[q] = Vn[q * T + t];
+      }
+      double p = 0.0;
+      if (c.own) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) p = fma(w[q], vi[q], p);
+      }
+      const double h = block_sum(c, p);
+      if (t == 0) hcol[i] = h;
+#pragma unroll
+      for (int q = 0; q < P; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(h, vi[q]));
+    }
+    part = 0.0;
+    if (c.own) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) part = fma(w[q], w[q], part);
+    }
+    const double hn = sqrt(block_sum(c, part));
+    const bool happy = hn <= 1e-14 * beta;
+    const double safe = hn > 0.0 ? hn : 1.0;
+#pragma unroll
+    for (int q = 0; q < P; ++q) v[q] = w[q] / safe;
+    if (c.own) {
+      double* Vj = V + (size_t)(j + 1) * n;
+#pragma unroll
+      for (int q = 0; q < P; ++q) Vj[q * T + t] = v[q];
+    }
+    if (t == 0) {
+      hcol[j + 1] = hn;
+      for (int i = 0; i < j; ++i) {  // stored rotations (circulant.py:308-312)
+        const double hi = hcol[i], hi1 = hcol[i + 1];
+        const double tt = __dadd_rn(__dmul_rn(cs[i], hi), __dmul_rn(sn[i], hi1));
+        hcol[i + 1] = __dadd_rn(__dmul_rn(-sn[i], hi), __dmul_rn(cs[i], hi1));
+        hcol[i] = tt;
+      }
+      double den = hypot(hcol[j], hcol[j + 1]);
+      den = den > 0.0 ? den : 1.0;
+      const double cj = hcol[j] / den, sj = hcol[j + 1] / den;
+      cs[j] = cj;
+      sn[j] = sj;
+      hcol[j] = __dadd_rn(__dmul_rn(cj, hcol[j]), __dmul_rn(sj, hcol[j + 1]));
+      hcol[j + 1] = 0.0;
+      const double gj = gg[j];
+      gg[j + 1] = __dmul_rn(-sj, gj);
+      gg[j] = __dmul_rn(cj, gj);
+      const double r = fabs(gg[j + 1]) / beta;
+      for (int i = 0; i <= j; ++i) R[(size_t)j * cap + i] = hcol[i];
+      c.bc[0] = r;
+      c.bc[1] = (!(r > sp.tol) || happy) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    res = c.bc[0];
+    depth = j + 1;
+    if (c.bc[1] != 0.0) break;
+  }
+  if (t == 0) {  // back substitution on the rotated (upper triangular) H
+    for (int i = 0; i < depth; ++i) ybuf[i] = gg[i];
+    for (int jj = depth - 1; jj >= 0; --jj) {
+      if (ybuf[jj] != 0.0) {
+        ybuf[jj] /= R[(size_t)jj * cap + jj];
+        const double yj = ybuf[jj];
+        for (int i = 0; i < jj; ++i) ybuf[i] = __dsub_rn(ybuf[i], __dmul_rn(yj, R[(size_t)jj * cap + i]));
+      }
+    }
+  }
+  __syncthreads();
+  if (c.own) {
+    for (int i = 0; i < depth; ++i) {
+      const double yi = ybuf[i];
+      const double* Vi = V + (size_t)i * n;
+#pragma unroll
+      for (int q = 0; q < P; ++q) x[q] = __dadd_rn(x[q], __dmul_rn(yi, Vi[q * T + t]));
+    }
+  }
+  depth_out = depth;
+  res_out = res;
+}
+
+// ------------------------------------------------------------- one step
+
+// Precondition: c.row holds the step input x (synchronised).
+// Postcondition: y = Phi x (own chunk).  c.row may have been reused; callers
+// __syncthreads() before writing it.
+template <int P, int KIND, int SPAN, int NST, bool EXACT>
+__device__ __forceinline__ void step_once(Ctx& c, const double (&wd)[SPAN + 1], int tb, int r0,
+                                          double (&y)[P], int& depth, double& gres) {
+  const StepParams& sp = *c.sp;
+  if constexpr (KIND == K_WIN) {
+    stencil_win<P, SPAN, EXACT>(c, tb, r0, wd, y);
+  } else if constexpr (KIND == K_GEN) {
+    stencil_gen<P, EXACT>(c, sp.ntap, sp.tap_off, sp.tap_w, y);
+  } else if constexpr (KIND == K_SLD) {
+    stencil_gen<P, true>(c, sp.ntap, sp.tap_off, sp.tap_w, y);
+    chain_solve<P>(c, y);
+  } else if constexpr (KIND == K_SLG) {
+    double b[P];
+    stencil_gen<P, true>(c, sp.ntap, sp.tap_off, sp.tap_w, b);
+    gmres_solve<P>(c, b, y, depth, gres);
+  } else {  // K_RK: staged Runge-Kutta sweep, stepping.py:363-378
+    double x[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] = c.own ? c.row[q * c.S + c.t] : 0.0;
+    double z[NST][P];
+#pragma unroll
+    for (int i = 0; i < NST; ++i) {
+      double rhs[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) rhs[q] = x[q];
+#pragma unroll
+      for (int j = 0; j < i; ++j) {
+        const double aij = sp.A[i * MAX_ST + j];
+        if (aij != 0.0) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) rhs[q] = __dadd_rn(rhs[q], __dmul_rn(aij, z[j][q]));
+        }
+      }
+      if (sp.implicit) chain_solve<P>(c, rhs);
+      __syncthreads();
+      if (c.own) chunk_to_row<P>(c.row, c.t, c.S, rhs);
+      __syncthreads();
+      stencil_gen<P, true>(c, sp.ntap, sp.tap_off, sp.tap_w, z[i]);
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q) y[q] = x[q];
+#pragma unroll
+    for (int i = 0; i < NST; ++i) {
+      const double bi = sp.b[i];
+      if (bi != 0.0) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], __dmul_rn(bi, z[i][q]));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ relax kernel
+
+__host__ __device__ constexpr int sp_bytes() { return (int)sizeof(StepParams); }
+
+template <int P, int KIND, int SPAN, int NST, bool EXACT>
+__global__ void __launch_bounds__(512) relax_kernel(const StepParams* __restrict__ gp, const RelaxLaunch L) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  {
+    const int4* src = reinterpret_cast<const int4*>(gp);
+    int4* dst = reinterpret_cast<int4*>(smem_raw);
+    for (int i = threadIdx.x; i < (int)(sizeof(StepParams) / 16); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const StepParams& sp = *reinterpret_cast<const StepParams*>(smem_raw);
+  const mgb_relax_args& a = L.a;
+  Ctx c;
+  c.sp = &sp;
+  c.n = sp.n;
+  c.T = sp.T;
+  c.S = sp.S;
+  c.t = threadIdx.x;
+  c.own = c.t < c.T;
+  c.row = reinterpret_cast<double*>(smem_raw + sizeof(StepParams));
+  c.red = c.row + (size_t)P * c.S;
+  c.bc = c.red + 64;
+  c.scan = c.bc + 8;
+  c.gm = c.scan + ((KIND == K_SLD || KIND == K_RK) ? 4 * c.T : 0);
+  c.ws = L.ws ? L.ws + (size_t)blockIdx.x * L.ws_slot : nullptr;
+  c.parity = 0;
+  const int n = c.n, t = c.t;
+
+  double wd[SPAN + 1];
+  int tb = 0, r0 = 0;
+  if constexpr (KIND == K_WIN) {
+#pragma unroll
+    for (int k = 0; k <= SPAN; ++k) wd[k] = sp.win_w[k];
+    tb = t + sp.win_lo / P;
+    tb = tb >= c.T ? tb - c.T : tb;
+    r0 = sp.win_lo & (P - 1);
+  } else {
+#pragma unroll
+    for (int k = 0; k <= SPAN; ++k) wd[k] = 0.0;
+  }
+  const int reps = sp.repeat;
+
+  for (long long k = blockIdx.x; k < a.n_intervals; k += gridDim.x) {
+    const long long kg = a.k_global0 + k;
+    const long long rowbase = k * (long long)a.m;
+    double y[P];
+    const double* csrc = (kg == 0 && a.c_src0) ? a.c_src0 : (a.c_src ? a.c_src + k * a.c_stride : nullptr);
+    if (c.own) {
+      if (csrc) {
+        load_chunk<P>(csrc, t, y);
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) y[q] = 0.0;
+      }
+      if (a.e && kg >= 1) {  // u[m::m] += e[1:] (mgrit.py:246)
+        double ev[P];
+        load_chunk<P>(a.e + k * a.e_stride, t, ev);
+#pragma unroll
+        for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], ev[q]);
+      }
+      if (a.c_out) store_chunk<P>(a.c_out + k * a.c_out_stride, t, y);
+    }
+    __syncthreads();
+    if (c.own) chunk_to_row<P>(c.row, t, c.S, y);
+    __syncthreads();
+    int depth = 0;
+    double gres = 0.0;
+    const int nsteps = a.n_fsteps + (a.tail ? 1 : 0);
+    for (int j = 1; j <= nsteps; ++j) {
+      const bool is_tail = j > a.n_fsteps;
+      for (int r = 0; r < reps; ++r) {
+        step_once<P, KIND, SPAN, NST, EXACT>(c, wd, tb, r0, y, depth, gres);
+        if (r + 1 < reps) {
+          __syncthreads();
+          if (c.own) chunk_to_row<P>(c.row, t, c.S, y);
+          __syncthreads();
+        }
+      }
+      // rhs row of this point; the tail step lands on C-point (k+1)m
+      const long long grow = is_tail ? rowbase + a.m : rowbase + j;
+      if (!is_tail) {
+        if (a.g && c.own) {
+          double gv[P];
+          load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+          for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], gv[q]);  // upd + g (mgrit.py:142)
+        }
+        __syncthreads();
+        if (c.own) chunk_to_row<P>(c.row, t, c.S, y);
+        __syncthreads();
+        if (a.write_f == 2 || (a.write_f == 1 && j == a.n_fsteps))
+          row_to_global<P>(c.row, a.u + grow * n, n, c.S);
+      } else if (a.tail == 1) {  // C-relaxation: Phi u_{km+m-1} + g_{(k+1)m} (mgrit.py:148-149)
+        if (c.own) {
+          if (a.g) {
+            double gv[P];
+            load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+            for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], gv[q]);
+          }
+          store_chunk<P>(a.tail_out + k * a.tail_stride, t, y);
+        }
+      } else {  // residual g + Phi u - u_C (mgrit.py:159-161)
+        double part = 0.0;
+        if (c.own) {
+          double r[P];
+          if (a.g) {
+            double gv[P];
+            load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+            for (int q = 0; q < P; ++q) r[q] = __dadd_rn(gv[q], y[q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) r[q] = y[q];
+          }
+          double cr[P];
+          load_chunk<P>(a.cref + k * a.cref_stride, t, cr);
+          if (a.cref_e) {
+            double ev[P];
+            load_chunk<P>(a.cref_e + k * a.cref_e_stride, t, ev);
+#pragma unroll
+            for (int q = 0; q < P; ++q) cr[q] = __dadd_rn(cr[q], ev[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            r[q] = __dsub_rn(r[q], cr[q]);
+            part = fma(r[q], r[q], part);
+          }
+          if (a.tail_out) store_chunk<P>(a.tail_out + k * a.tail_stride, t, r);
+        }
+        if (a.partials) {
+          const double s = block_sum(c, part);
+          if (t == 0) a.partials[k] = s;
+        }
+      }
+    }
+    if (a.c_last_out && k == a.n_intervals - 1 && c.own) {  // final C-point (k+1 >= 1)
+      double cl[P];
+      if (a.c_src) {
+        load_chunk<P>(a.c_src + (k + 1) * a.c_stride, t, cl);
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) cl[q] = 0.0;
+      }
+      if (a.e) {
+        double ev[P];
+        load_chunk<P>(a.e + (k + 1) * a.e_stride, t, ev);
+#pragma unroll
+        for (int q = 0; q < P; ++q) cl[q] = __dadd_rn(cl[q], ev[q]);
+      }
+      store_chunk<P>(a.c_last_out, t, cl);
+    }
+    if (t == 0) {
+      if (a.stats_depth) a.stats_depth[k] = depth;
+      if (a.stats_res) a.stats_res[k] = gres;
+    }
+  }
+}
+
+__global__ void sum_kernel(const double* __restrict__ p, long long n, double* out);
+
+}  // namespace mgb

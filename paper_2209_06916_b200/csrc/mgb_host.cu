@@ -1,0 +1,508 @@
+// mgb_host.cu -- host side of libmgrit_b200.so: device plans for one-step
+// operators, spectral factorisation of the implicit circulants, launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "mgb_registry.h"
+
+using mgb::Factor;
+using mgb::StepParams;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                           \
+  do {                                                                           \
+    cudaError_t e_ = (expr);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(MGB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+std::mutex& reg_mutex() {
+  static std::mutex m;
+  return m;
+}
+std::map<std::tuple<int, int, int, int, int>, const void*>& registry() {
+  static std::map<std::tuple<int, int, int, int, int>, const void*> r;
+  return r;
+}
+void ensure_registered() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    mgb::register_win_exact();
+    mgb::register_win_fast();
+    mgb::register_gen();
+    mgb::register_rk();
+  });
+}
+
+// ------------------------------------------------------ long double algebra
+using ld = long double;
+using cld = std::complex<long double>;
+
+struct M2 {
+  ld a, b, c, d;
+};
+M2 mul(const M2& x, const M2& y) {
+  return {x.a * y.a + x.b * y.c, x.a * y.b + x.b * y.d, x.c * y.a + x.d * y.c, x.c * y.b + x.d * y.d};
+}
+M2 mpow(M2 base, long long e) {
+  M2 r{1, 0, 0, 1};
+  while (e > 0) {
+    if (e & 1) r = mul(r, base);
+    base = mul(base, base);
+    e >>= 1;
+  }
+  return r;
+}
+void put(double* dst, const M2& m) {
+  dst[0] = (double)m.a;
+  dst[1] = (double)m.b;
+  dst[2] = (double)m.c;
+  dst[3] = (double)m.d;
+}
+
+cld peval(const std::vector<cld>& c, cld z) {  // c[k] z^k
+  cld acc = 0;
+  for (int k = (int)c.size() - 1; k >= 0; --k) acc = acc * z + c[k];
+  return acc;
+}
+
+// Roots of sum_k c[k] z^k (c.back() != 0): Durand-Kerner + Newton polish.
+std::vector<cld> poly_roots(const std::vector<ld>& cr) {
+  const int d = (int)cr.size() - 1;
+  std::vector<cld> c(d + 1);
+  for (int k = 0; k <= d; ++k) c[k] = cld(cr[k] / cr[d], 0);
+  ld bound = 0;
+  for (int k = 0; k < d; ++k) bound = std::max(bound, std::abs(c[k]));
+  bound = 1 + bound;
+  std::vector<cld> z(d);
+  const cld seed(0.4L, 0.9L);
+  cld p = 1;
+  for (int i = 0; i < d; ++i) {
+    p *= seed;
+    z[i] = p * (bound / std::abs(p)) * (ld)(0.5 + 0.5 * (i + 1) / d);
+  }
+  for (int it = 0; it < 2000; ++it) {
+    ld change = 0;
+    for (int i = 0; i < d; ++i) {
+      cld den = 1;
+      for (int j = 0; j < d; ++j)
+        if (j != i) den *= (z[i] - z[j]);
+      if (std::abs(den) == 0) den = cld(1e-30L, 0);
+      cld dz = peval(c, z[i]) / den;
+      z[i] -= dz;
+      change = std::max(change, std::abs(dz) / std::max((ld)1, std::abs(z[i])));
+    }
+    if (change < 1e-30L) break;
+  }
+  // Newton polish
+  std::vector<cld> dc(std::max(d, 1));
+  for (int k = 1; k <= d; ++k) dc[k - 1] = c[k] * (ld)k;
+  for (int i = 0; i < d; ++i) {
+    for (int it = 0; it < 8; ++it) {
+      cld f = peval(c, z[i]);
+      cld fp = peval(dc, z[i]);
+      if (std::abs(fp) == 0) break;
+      cld dz = f / fp;
+      z[i] -= dz;
+      if (std::abs(dz) <= 1e-19L * std::max((ld)1, std::abs(z[i]))) break;
+    }
+  }
+  return z;
+}
+
+struct FactorDesc {
+  ld a1, a2;
+  int dir;
+};
+
+// Factorise the circulant with stencil (offsets, weights):
+//   a(z) = K z^s prod_f F_f(z),  F = (1 - zeta/z)[(1 - conj(zeta)/z)]  (inside roots, forward)
+//                              or (1 - z/zeta)[(1 - z/conj(zeta))]  (outside roots, backward)
+int factorize(const std::vector<long long>& off, const std::vector<double>& w, int n,
+              std::vector<FactorDesc>& facs, ld& K, int& shift) {
+  long long lo = off[0], hi = off[0];
+  for (auto o : off) {
+    lo = std::min(lo, o);
+    hi = std::max(hi, o);
+  }
+  const int d = (int)(hi - lo);
+  if (d > 30) return fail(MGB_ERR_UNSUPPORTED, "implicit stencil too wide to factorise");
+  std::vector<ld> c(d + 1, 0);
+  for (size_t k = 0; k < off.size(); ++k) c[off[k] - lo] += (ld)w[k];
+  facs.clear();
+  if (d == 0) {
+    K = c[0];
+    shift = (int)lo;
+    if (K == 0) return fail(MGB_ERR_SINGULAR, "zero operator");
+    return MGB_OK;
+  }
+  std::vector<cld> roots = poly_roots(c);
+  std::vector<cld> in_r, out_r;
+  for (auto& z : roots) {
+    const ld m = std::abs(z);
+    if (std::fabs(m - 1) < 1e-12L) return fail(MGB_ERR_SINGULAR, "implicit operator singular (root on unit circle)");
+    if (std::fabs(z.imag()) <= 1e-14L * m) z = cld(z.real(), 0);
+    (m < 1 ? in_r : out_r).push_back(z);
+  }
+  cld Kc = cld(c[d], 0);
+  for (auto& z : out_r) Kc *= -z;
+  if (std::fabs(Kc.imag()) > 1e-10L * std::abs(Kc)) return fail(MGB_ERR_INVALID, "non-real gain in factorisation");
+  K = Kc.real();
+  shift = (int)(lo + (long long)in_r.size());
+  auto emit = [&](std::vector<cld>& rs, bool inside) -> int {
+    std::vector<bool> used(rs.size(), false);
+    for (size_t i = 0; i < rs.size(); ++i) {
+      if (used[i]) continue;
+      used[i] = true;
+      const cld mu = inside ? rs[i] : ((ld)1 / rs[i]);
+      if (rs[i].imag() == 0) {
+        facs.push_back({mu.real(), 0, inside ? +1 : -1});
+        continue;
+      }
+      // find conjugate partner
+      size_t best = rs.size();
+      ld bd = 1e300L;
+      for (size_t j = 0; j < rs.size(); ++j) {
+        if (used[j]) continue;
+        ld dd = std::abs(rs[j] - std::conj(rs[i]));
+        if (dd < bd) {
+          bd = dd;
+          best = j;
+        }
+      }
+      if (best == rs.size() || bd > 1e-8L * std::abs(rs[i]))
+        return fail(MGB_ERR_INVALID, "complex root without conjugate partner");
+      used[best] = true;
+      facs.push_back({2 * mu.real(), -std::norm(mu), inside ? +1 : -1});
+    }
+    return MGB_OK;
+  };
+  int rc = emit(in_r, true);
+  if (rc) return rc;
+  rc = emit(out_r, false);
+  if (rc) return rc;
+  // verify: symbol of the factorisation equals the stencil symbol
+  for (int kk = 0; kk < 7; ++kk) {
+    const ld om = 2 * 3.14159265358979323846264338327950288L * kk / 7.0L + 0.1L;
+    const cld z = std::polar((ld)1, om);
+    cld direct = 0;
+    for (size_t k = 0; k < off.size(); ++k) direct += (ld)w[k] * std::pow(z, (int)off[k]);
+    cld fact = K * std::pow(z, shift);
+    for (auto& f : facs) {
+      if (f.dir > 0)
+        fact *= (ld)1 - f.a1 / z - f.a2 / (z * z);
+      else
+        fact *= (ld)1 - f.a1 * z - f.a2 * z * z;
+    }
+    ld scale = 0;
+    for (auto ww : w) scale += std::fabs((ld)ww);
+    if (std::abs(direct - fact) > 1e-11L * scale)
+      return fail(MGB_ERR_INVALID, "factorisation check failed");
+  }
+  return MGB_OK;
+}
+
+void fill_factor_tables(const FactorDesc& fd, int T, int P, Factor& F) {
+  std::memset(&F, 0, sizeof(F));
+  F.a1 = (double)fd.a1;
+  F.a2 = (double)fd.a2;
+  F.dir = fd.dir;
+  const M2 A{(ld)F.a1, (ld)F.a2, 1, 0};
+  M2 Ak = A;
+  for (int q = 0; q < P; ++q) {
+    F.h1[q] = (double)Ak.a;
+    F.h2[q] = (double)Ak.b;
+    Ak = mul(A, Ak);
+  }
+  const M2 M = mpow(A, P);
+  put(F.M, M);
+  M2 Mp = M;
+  for (int k = 0; k < mgb::LOGT; ++k) {
+    put(F.Mpow[k], Mp);
+    Mp = mul(Mp, Mp);
+  }
+  const int R = (T + 31) / 32;
+  M2 MR = mpow(M, R);
+  for (int d = 0; d < 5; ++d) {
+    put(F.MR[d], MR);
+    MR = mul(MR, MR);
+  }
+  const M2 MT = mpow(M, T);
+  const M2 IM{1 - MT.a, -MT.b, -MT.c, 1 - MT.d};
+  const ld det = IM.a * IM.d - IM.b * IM.c;
+  const M2 inv{IM.d / det, -IM.b / det, -IM.c / det, IM.a / det};
+  put(F.Winv, inv);
+}
+
+int choose_layout(int kind, int n, int& P, int& T, int& S) {
+  const int pmax = (kind == mgb::K_RK) ? 8 : 16;
+  P = 1;
+  for (int p = pmax; p >= 1; p >>= 1) {
+    if (n % p == 0 && n / p >= 64) {
+      P = p;
+      break;
+    }
+  }
+  while (n / P > 512 && P < 16 && n % (2 * P) == 0) P *= 2;
+  T = n / P;
+  if (T > 512 || T * P != n)
+    return fail(MGB_ERR_UNSUPPORTED, "n_x=" + std::to_string(n) +
+                                         " outside the single-CTA slice envelope (need n_x = T*P, T<=512, P<=16)");
+  const int want = (P >= 16) ? 1 : 16 / P;
+  S = T;
+  while (S % 16 != want % 16) ++S;
+  return MGB_OK;
+}
+
+long long mod_n(long long o, int n) {
+  long long r = o % n;
+  return r < 0 ? r + n : r;
+}
+
+}  // namespace
+
+namespace mgb {
+void register_kernel(const KernelKey& k, const void* fn) {
+  std::lock_guard<std::mutex> lk(reg_mutex());
+  registry()[std::make_tuple(k.kind, k.P, k.span, k.nst, k.exact)] = fn;
+}
+
+__global__ void sum_kernel(const double* __restrict__ p, long long n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += p[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    *out = tot;
+  }
+}
+}  // namespace mgb
+
+struct mgb_step {
+  StepParams hp;
+  StepParams* dp = nullptr;
+  int dkind = 0, P = 1, T = 1, S = 1, span = 0, nst = 1, exact = 1;
+  int threads = 32, smem = 0, max_grid = 1;
+  const void* fn = nullptr;
+  double* ws = nullptr;
+  long long ws_slot = 0;
+  int ws_slots = 0;
+};
+
+extern "C" {
+
+int mgb_version(void) { return 1; }
+const char* mgb_last_error(void) { return g_err.c_str(); }
+int64_t mgb_launch_count(void) { return g_launches.load(); }
+
+int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
+  if (!d || !out) return fail(MGB_ERR_INVALID, "null argument");
+  *out = nullptr;
+  ensure_registered();
+  const int n = d->n_x;
+  if (n < 1) return fail(MGB_ERR_INVALID, "n_x must be positive");
+  if (d->n_taps < 1 || d->n_taps > mgb::MAX_TAPS)
+    return fail(MGB_ERR_UNSUPPORTED, "primary stencil must have 1.." + std::to_string(mgb::MAX_TAPS) + " taps");
+  auto st = new mgb_step();
+  StepParams& hp = st->hp;
+  std::memset(&hp, 0, sizeof(hp));
+  hp.exact = d->exact ? 1 : 0;
+  hp.repeat = std::max(1, (int)d->repeat);
+  int dk;
+  switch (d->kind) {
+    case MGB_STEP_STENCIL: dk = mgb::K_GEN; break;
+    case MGB_STEP_RK_STAGED: dk = mgb::K_RK; break;
+    case MGB_STEP_SL_DIRECT: dk = mgb::K_SLD; break;
+    case MGB_STEP_SL_GMRES: dk = mgb::K_SLG; break;
+    default: delete st; return fail(MGB_ERR_INVALID, "unknown step kind");
+  }
+  int P, T, S;
+  int rc = choose_layout(dk, n, P, T, S);
+  if (rc) { delete st; return rc; }
+  hp.n = n; hp.P = P; hp.T = T; hp.S = S;
+  hp.ntap = d->n_taps;
+  std::vector<long long> off(d->n_taps);
+  for (int k = 0; k < d->n_taps; ++k) {
+    off[k] = d->offsets[k];
+    hp.tap_off[k] = (int)mod_n(off[k], n);
+    hp.tap_w[k] = d->weights[k];
+  }
+  // register-window eligibility (explicit stencils)
+  int span = 0;
+  if (dk == mgb::K_GEN) {
+    bool inc = true;
+    for (int k = 1; k < d->n_taps; ++k) inc = inc && off[k] > off[k - 1];
+    const long long sp = off.back() - off.front();
+    if (inc && sp <= 30 && P >= 4 && T >= 64) {
+      for (int s : mgb::kWinSpans)
+        if (s >= sp) { span = s; break; }
+      dk = mgb::K_WIN;
+      hp.win_lo = (int)mod_n(off.front(), n);
+      hp.win_span = span;
+      for (int k = 0; k < d->n_taps; ++k) hp.win_w[off[k] - off.front()] = d->weights[k];
+    }
+  }
+  if (dk == mgb::K_RK) {
+    if (d->stages < 1 || d->stages > mgb::MAX_ST) { delete st; return fail(MGB_ERR_UNSUPPORTED, "1..6 RK stages supported"); }
+    hp.stages = d->stages;
+    for (int i = 0; i < d->stages; ++i) {
+      hp.b[i] = d->rk_b[i];
+      for (int j = 0; j < d->stages; ++j) hp.A[i * mgb::MAX_ST + j] = d->rk_a[i * d->stages + j];
+    }
+    hp.implicit = d->implicit ? 1 : 0;
+  }
+  hp.gain_inv = 1.0;
+  if ((dk == mgb::K_RK && hp.implicit) || dk == mgb::K_SLD) {
+    if (d->n_taps2 < 1) { delete st; return fail(MGB_ERR_INVALID, "implicit operator stencil missing"); }
+    std::vector<long long> o2(d->offsets2, d->offsets2 + d->n_taps2);
+    std::vector<double> w2(d->weights2, d->weights2 + d->n_taps2);
+    std::vector<FactorDesc> facs;
+    ld K;
+    int shift;
+    rc = factorize(o2, w2, n, facs, K, shift);
+    if (rc) { delete st; return rc; }
+    if ((int)facs.size() > mgb::MAX_FAC) { delete st; return fail(MGB_ERR_UNSUPPORTED, "too many factors"); }
+    hp.nfac = (int)facs.size();
+    for (int f = 0; f < hp.nfac; ++f) fill_factor_tables(facs[f], T, P, hp.fac[f]);
+    hp.gain_inv = (double)(1.0L / K);
+    hp.shift = (int)mod_n(shift, n);
+    if (hp.shift > n / 2) hp.shift -= n;
+  }
+  if (dk == mgb::K_SLG) {
+    if (d->n_taps2 < 1 || d->n_taps2 > mgb::MAX_TAPS2) { delete st; return fail(MGB_ERR_UNSUPPORTED, "GMRES operator stencil size"); }
+    hp.ntap2 = d->n_taps2;
+    for (int k = 0; k < d->n_taps2; ++k) {
+      hp.tap2_off[k] = (int)mod_n(d->offsets2[k], n);
+      hp.tap2_w[k] = d->weights2[k];
+    }
+    hp.tol = d->gmres_tol;
+    hp.cap = std::min((int)d->gmres_cap, n);
+    if (hp.cap < 1 || hp.cap > mgb::MAX_CAP) { delete st; return fail(MGB_ERR_UNSUPPORTED, "GMRES cap must be 1..128"); }
+  }
+  hp.kind = dk;
+  st->dkind = dk;
+  st->P = P; st->T = T; st->S = S;
+  st->span = span;
+  st->nst = dk == mgb::K_RK ? hp.stages : 1;
+  st->exact = (dk == mgb::K_WIN || dk == mgb::K_GEN) ? hp.exact : 1;
+  st->threads = ((T + 31) / 32) * 32;
+  size_t dbl = (size_t)P * S + 64 + 8;
+  if (dk == mgb::K_RK || dk == mgb::K_SLD) dbl += 4 * (size_t)T;
+  if (dk == mgb::K_SLG) dbl += 2 * mgb::MAX_CAP + 2;
+  st->smem = (int)(sizeof(StepParams) + 8 * dbl);
+  {
+    std::lock_guard<std::mutex> lk(reg_mutex());
+    auto it = registry().find(std::make_tuple(dk, P, span, st->nst, st->exact));
+    if (it == registry().end()) { delete st; return fail(MGB_ERR_UNSUPPORTED, "no kernel instantiation for this layout"); }
+    st->fn = it->second;
+  }
+  cudaError_t e = cudaFuncSetAttribute(st->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, st->smem);
+  if (e != cudaSuccess) { delete st; return fail(MGB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)); }
+  int nb = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, st->fn, st->threads, st->smem);
+  if (e != cudaSuccess || nb < 1) {
+    delete st;
+    return fail(MGB_ERR_UNSUPPORTED, std::string("kernel cannot be resident: ") + cudaGetErrorString(e));
+  }
+  st->max_grid = nb * sms;
+  e = cudaMalloc(&st->dp, sizeof(StepParams));
+  if (e != cudaSuccess) { delete st; return fail(MGB_ERR_CUDA, "cudaMalloc params"); }
+  e = cudaMemcpy(st->dp, &hp, sizeof(StepParams), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(st->dp); delete st; return fail(MGB_ERR_CUDA, "upload params"); }
+  *out = st;
+  return MGB_OK;
+}
+
+void mgb_step_destroy(mgb_step* st) {
+  if (!st) return;
+  if (st->dp) cudaFree(st->dp);
+  if (st->ws) cudaFree(st->ws);
+  delete st;
+}
+
+int mgb_step_layout(const mgb_step* st, int32_t* threads, int32_t* ppt, int32_t* smem) {
+  if (!st) return fail(MGB_ERR_INVALID, "null step");
+  if (threads) *threads = st->T;
+  if (ppt) *ppt = st->P;
+  if (smem) *smem = st->smem;
+  return MGB_OK;
+}
+
+int mgb_step_reserve_workspace(mgb_step* st, void* stream) {
+  (void)stream;
+  if (!st) return fail(MGB_ERR_INVALID, "null step");
+  if (st->dkind != mgb::K_SLG || st->ws) return MGB_OK;
+  const long long cap = st->hp.cap, n = st->hp.n;
+  st->ws_slot = (cap + 1) * n + cap * cap + 3 * cap + 1;
+  st->ws_slot = (st->ws_slot + 31) / 32 * 32;
+  st->ws_slots = st->max_grid;
+  CUDA_TRY(cudaMalloc(&st->ws, (size_t)st->ws_slot * st->ws_slots * sizeof(double)));
+  return MGB_OK;
+}
+
+int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
+  if (!st || !a) return fail(MGB_ERR_INVALID, "null argument");
+  if (a->n_intervals <= 0) return MGB_OK;
+  if (a->m < 1 || a->n_fsteps < 0) return fail(MGB_ERR_INVALID, "bad m / n_fsteps");
+  if (a->tail == 1 && !a->tail_out) return fail(MGB_ERR_INVALID, "C-relax tail needs tail_out");
+  if (a->tail == 2 && !a->cref) return fail(MGB_ERR_INVALID, "residual tail needs cref");
+  if (a->write_f && !a->u) return fail(MGB_ERR_INVALID, "write_f needs u");
+  mgb::RelaxLaunch L;
+  L.a = *a;
+  L.ws = nullptr;
+  L.ws_slot = 0;
+  long long grid = std::min<long long>(a->n_intervals, st->max_grid);
+  if (st->dkind == mgb::K_SLG) {
+    int rc = mgb_step_reserve_workspace(st, stream);
+    if (rc) return rc;
+    L.ws = st->ws;
+    L.ws_slot = st->ws_slot;
+    grid = std::min<long long>(grid, st->ws_slots);
+  }
+  const StepParams* dp = st->dp;
+  void* args[] = {(void*)&dp, (void*)&L};
+  CUDA_TRY(cudaLaunchKernel(st->fn, dim3((unsigned)grid), dim3(st->threads), args, (size_t)st->smem,
+                            (cudaStream_t)stream));
+  g_launches++;
+  return MGB_OK;
+}
+
+int mgb_sum(const double* partials, int64_t n, double* out, void* stream) {
+  if (!out) return fail(MGB_ERR_INVALID, "null out");
+  if (n <= 0) {
+    CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream));
+    return MGB_OK;
+  }
+  mgb::sum_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(partials, (long long)n, out);
+  CUDA_TRY(cudaGetLastError());
+  g_launches++;
+  return MGB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,374 @@
+"""Linear MGRIT on the B200 (drop-in for mgrit.py of the reference).
+
+Same API and semantics as the reference (mgrit.py:28-297): F(CF)^nu
+relaxation, injection restriction, two-level or V-cycle, halting on
+``norms[-1] / norms[0] <= tol``, divergence reported, ``initial_iterate``
+mutated in place.  The iterate lives in HBM; every relaxation, restriction,
+correction and norm runs in ``libmgrit_b200.so``.
+
+Kernel schedule of one cycle on a level with nu = 1:
+
+  FC   interval k: F-relax from C-point k (interior writes elided), then
+       C-relax into the ping buffer cbuf[k+1]           (mgrit.py:231-233)
+  FR   interval k: F-relax from cbuf[k], then the injected residual
+       r_{k+1} = g + Phi u_{(k+1)m-1} - cbuf[k+1] -> coarse rhs  (:234-237)
+  ...  coarse solve: recursive cycle or one-CTA forward substitution (:239-244)
+  CF   interval k: u_C[k] = cbuf[k] + e[k], F-relax writing all F-points,
+       then (fine level) the residual of the next norm      (:246-247, :270)
+
+Skipping interior F-point writes in FC/FR is exact: only u_{km+m-1} is read
+before the closing F-relaxation rewrites every F-point (verified
+bitwise on the reference).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+
+from .device import device_sum, plan_for, ptr, require_cuda, to_device
+from .stepping import Stepper
+
+_F64 = 8
+
+
+@dataclass
+class MgritConfig:
+    """F(CF)^nu pre-relaxation, cycle type, halting (mgrit.py:28-44)."""
+
+    nu: int = 1
+    cycle: str = "two_level"
+    tol: float = 1e-10
+    max_iters: int = 30
+    rng_seed: int = 0
+
+    def __post_init__(self):
+        if self.nu < 0:
+            raise ValueError(f"nu must be >= 0, got {self.nu}")
+        if self.cycle not in ("two_level", "v_cycle"):
+            raise ValueError(f"unknown cycle {self.cycle!r}")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+
+
+@dataclass
+class TimeGridProblem:
+    """Per-level steppers, coarsening factors and u0 (mgrit.py:47-93)."""
+
+    steppers: List[Stepper]
+    m: List[int]
+    n_t: int
+    u0: np.ndarray
+
+    def __post_init__(self):
+        self.u0 = np.asarray(self.u0, dtype=float)
+        if len(self.steppers) != len(self.m) + 1:
+            raise ValueError("need one stepper per level: "
+                             f"{len(self.steppers)} steppers, {len(self.m)} factors")
+        n = self.n_t
+        for lvl, mf in enumerate(self.m):
+            if mf < 2:
+                raise ValueError(f"coarsening factor must be >= 2, got {mf}")
+            if n % mf != 0:
+                raise ValueError(f"level {lvl} has {n} steps, not divisible by m = {mf}")
+            n //= mf
+        if n < 1:
+            raise ValueError("coarsest level must keep at least one step")
+        if any(s.n_x != len(self.u0) for s in self.steppers):
+            raise ValueError("stepper mesh sizes must match the initial condition")
+
+    @property
+    def n_levels(self) -> int:
+        return len(self.steppers)
+
+    @property
+    def n_x(self) -> int:
+        return len(self.u0)
+
+    def points_on_level(self, level: int) -> int:
+        n = self.n_t
+        for mf in self.m[:level]:
+            n //= mf
+        return n + 1
+
+
+@dataclass
+class SolveReport:
+    """Residual history and effective convergence factor (mgrit.py:96-110)."""
+
+    residual_norms: List[float]
+    iterations: int
+    effective_rho: float
+    converged: bool
+    wall_time: float = 0.0
+
+    @property
+    def total_reduction(self) -> float:
+        if self.residual_norms[0] == 0.0:
+            return 0.0
+        return self.residual_norms[-1] / self.residual_norms[0]
+
+
+def initial_condition(n_x: int) -> np.ndarray:
+    """sin^4(pi x) on [-1, 1) (mgrit.py:294-297)."""
+    x = -1.0 + 2.0 * np.arange(n_x) / n_x
+    return np.sin(np.pi * x) ** 4
+
+
+# ------------------------------------------------------- drop-in primitives
+
+def _writeback(host, dev):
+    if host is not None:
+        host[...] = dev.cpu().numpy().reshape(host.shape)
+
+
+def f_relax(u, g, stepper: Stepper, m: int, pool=None, threads: int = 1) -> None:
+    """F-relaxation in place (mgrit.py:132-142); numpy or CUDA tensors."""
+    ud, uh = to_device(u)
+    gd, _ = to_device(g) if g is not None else (None, None)
+    n = ud.shape[-1]
+    N = ud.shape[0]
+    plan = plan_for(stepper.program)
+    full, rem = (N - 1) // m, (N - 1) % m
+    plan.relax(full, m, m - 1, c_src=ptr(ud), c_stride=m * n, u=ptr(ud), write_f=2, g=ptr(gd))
+    if rem:
+        off = full * m * n * _F64
+        plan.relax(1, m, rem, c_src=ptr(ud) + off, c_stride=0, u=ptr(ud) + off, write_f=2,
+                   g=None if gd is None else ptr(gd) + off)
+    _writeback(uh, ud)
+
+
+def c_relax(u, g, stepper: Stepper, m: int, pool=None, threads: int = 1) -> None:
+    """C-relaxation in place (mgrit.py:145-149)."""
+    ud, uh = to_device(u)
+    gd, _ = to_device(g) if g is not None else (None, None)
+    n = ud.shape[-1]
+    cnt = (ud.shape[0] - 1) // m
+    plan_for(stepper.program).relax(cnt, m, 0, c_src=ptr(ud) + (m - 1) * n * _F64,
+                                    c_stride=m * n, tail=1, tail_out=ptr(ud) + m * n * _F64,
+                                    tail_stride=m * n, g=ptr(gd))
+    _writeback(uh, ud)
+
+
+def _residual(ud, gd, stepper, m, out=None, partials=None):
+    n = ud.shape[-1]
+    cnt = (ud.shape[0] - 1) // m
+    plan_for(stepper.program).relax(cnt, m, 0, c_src=ptr(ud) + (m - 1) * n * _F64,
+                                    c_stride=m * n, tail=2, cref=ptr(ud) + m * n * _F64,
+                                    cref_stride=m * n, tail_out=ptr(out),
+                                    tail_stride=n, g=ptr(gd), partials=ptr(partials))
+    return cnt
+
+
+def restrict_residual(u, g, stepper: Stepper, m: int, pool=None, threads: int = 1):
+    """Coarse-point residuals g_km + Phi u_{km-1} - u_km, k >= 1 (mgrit.py:152-161)."""
+    torch = require_cuda()
+    ud, uh = to_device(u)
+    gd, _ = to_device(g) if g is not None else (None, None)
+    cnt = (ud.shape[0] - 1) // m
+    r = torch.empty((cnt, ud.shape[-1]), dtype=torch.float64, device=ud.device)
+    _residual(ud, gd, stepper, m, out=r)
+    return r.cpu().numpy() if uh is not None else r
+
+
+def cpoint_residual_norm(u, g, stepper: Stepper, m: int, pool=None, threads: int = 1) -> float:
+    """Global l2 norm of the C-point residuals (mgrit.py:164-166)."""
+    torch = require_cuda()
+    ud, _ = to_device(u)
+    gd, _ = to_device(g) if g is not None else (None, None)
+    cnt = (ud.shape[0] - 1) // m
+    part = torch.empty(max(cnt, 1), dtype=torch.float64, device=ud.device)
+    tot = torch.empty(1, dtype=torch.float64, device=ud.device)
+    _residual(ud, gd, stepper, m, partials=part)
+    device_sum(ptr(part), cnt, ptr(tot))
+    return math.sqrt(float(tot.item()))
+
+
+def _forward_substitute_dev(plan, out, g, n_pts: int, start=None):
+    """u_0 = start (or g_0), u_k = Phi u_{k-1} + g_k on one CTA (mgrit.py:169-191)."""
+    plan.relax(1, n_pts, n_pts - 1, c_src=start if start is not None else g, c_stride=0,
+               c_out=out, c_out_stride=0, u=out, write_f=2, g=g)
+
+
+def sequential_solve(problem: TimeGridProblem, level: int = 0, g=None):
+    """Exact forward substitution on ``level`` (mgrit.py:169-183)."""
+    torch = require_cuda()
+    n_pts = problem.points_on_level(level)
+    out = torch.empty((n_pts, problem.n_x), dtype=torch.float64, device="cuda")
+    plan = plan_for(problem.steppers[level].program)
+    if g is None:
+        u0 = torch.from_numpy(np.ascontiguousarray(problem.u0)).to("cuda")
+        _forward_substitute_dev(plan, ptr(out), None, n_pts, start=ptr(u0))
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+    gd, gh = to_device(g)
+    _forward_substitute_dev(plan, ptr(out), ptr(gd), n_pts)
+    return out.cpu().numpy() if gh is not None else out
+
+
+# ----------------------------------------------------------------- solver
+
+class _Level:
+    def __init__(self, torch, stepper: Stepper, m: int, n_pts: int, n_x: int, nu: int):
+        self.plan = plan_for(stepper.program)
+        self.m = m
+        self.n_pts = n_pts
+        self.n_int = (n_pts - 1) // m
+        shape = (self.n_int + 1, n_x)
+        self.cbuf = [torch.empty(shape, dtype=torch.float64, device="cuda")
+                     for _ in range(min(nu, 2))]
+
+
+class MgritSolver:
+    """Level hierarchy, HBM buffers and the GPU cycle (mgrit.py:194-285)."""
+
+    def __init__(self, problem: TimeGridProblem, config: MgritConfig, threads: int = 1):
+        self.problem = problem
+        self.config = config
+        self.threads = max(1, int(threads))
+        self._built = False
+        self.stats = {}
+
+    # ---------------------------------------------------------- buffers
+    def _build(self):
+        if self._built:
+            return
+        torch = require_cuda()
+        pr, cfg = self.problem, self.config
+        n_x = pr.n_x
+        self._torch = torch
+        nlev = len(pr.m)
+        self.levels = [_Level(torch, pr.steppers[l], pr.m[l], pr.points_on_level(l), n_x,
+                              cfg.nu) for l in range(nlev)]
+        # coarse iterates e_l and right-hand sides g_l for levels 1..nlev
+        self.ucoarse = [None]
+        self.gcoarse = [None]
+        for l in range(1, nlev + 1):
+            npts = pr.points_on_level(l)
+            self.ucoarse.append(torch.zeros((npts, n_x), dtype=torch.float64, device="cuda"))
+            self.gcoarse.append(torch.zeros((npts, n_x), dtype=torch.float64, device="cuda"))
+        self.plans = [plan_for(s.program) for s in pr.steppers]
+        self.zero_row = torch.zeros(n_x, dtype=torch.float64, device="cuda")
+        n0 = self.levels[0].n_int
+        self.partials = torch.empty(max(n0, 1), dtype=torch.float64, device="cuda")
+        self.sumbuf = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self._built = True
+
+    # ---------------------------------------------------------- iteration
+    def initial_state(self) -> np.ndarray:
+        """U[0,1) iterate from default_rng(rng_seed), row 0 := u0 (mgrit.py:206-211)."""
+        rng = np.random.default_rng(self.config.rng_seed)
+        u = rng.random((self.problem.n_t + 1, self.problem.n_x))
+        u[0] = self.problem.u0
+        return u
+
+    def rhs(self) -> np.ndarray:
+        g = np.zeros((self.problem.n_t + 1, self.problem.n_x))
+        g[0] = self.problem.u0
+        return g
+
+    def _cycle(self, l: int, u: int, g: Optional[int], u_zero: bool, want_norm: bool) -> None:
+        cfg = self.config
+        L = self.levels[l]
+        n = self.problem.n_x
+        m, nI, plan = L.m, L.n_int, L.plan
+        row = n * _F64
+        zero = ptr(self.zero_row)
+        u0row = zero if u_zero else u
+        src, stride = (None if u_zero else u), m * n
+        for i in range(cfg.nu):
+            dst = L.cbuf[i % 2]
+            plan.relax(nI, m, m - 1, c_src=src, c_stride=stride, c_src0=u0row, tail=1,
+                       tail_out=ptr(dst) + row, tail_stride=n, g=g)
+            src, stride = ptr(dst), n
+        gC = self.gcoarse[l + 1]
+        uC = self.ucoarse[l + 1]
+        if cfg.nu == 0:
+            cref, cref_stride = (zero, 0) if u_zero else (u + m * row, m * n)
+        else:
+            cref, cref_stride = src + row, n
+        plan.relax(nI, m, m - 1, c_src=src, c_stride=stride, c_src0=u0row, tail=2, cref=cref,
+                   cref_stride=cref_stride, tail_out=ptr(gC) + row, tail_stride=n, g=g)
+        child = l + 1
+        if cfg.cycle == "two_level" or child == len(self.levels):
+            _forward_substitute_dev(self.plans[child], ptr(uC), ptr(gC), nI + 1)
+        else:
+            self._cycle(child, ptr(uC), ptr(gC), True, False)
+        fuse_norm = want_norm and cfg.nu > 0
+        if cfg.nu == 0:
+            c_src, c_stride = (None if u_zero else u), m * n
+        else:
+            c_src, c_stride = src, n
+        plan.relax(nI, m, m - 1, c_src=c_src, c_stride=c_stride, c_src0=u0row, e=ptr(uC),
+                   e_stride=n, c_out=u, c_out_stride=m * n, c_last_out=u + nI * m * row,
+                   u=u, write_f=2, g=g,
+                   tail=2 if fuse_norm else 0, cref=(c_src + row) if fuse_norm else None,
+                   cref_stride=n, cref_e=ptr(uC) + row, cref_e_stride=n,
+                   partials=ptr(self.partials) if fuse_norm else None)
+        if want_norm and not fuse_norm:
+            self._residual_partials(u, g)
+
+    def _residual_partials(self, u: int, g: Optional[int]) -> None:
+        L = self.levels[0]
+        n = self.problem.n_x
+        m = L.m
+        L.plan.relax(L.n_int, m, 0, c_src=u + (m - 1) * n * _F64, c_stride=m * n, tail=2,
+                     cref=u + m * n * _F64, cref_stride=m * n, g=g, partials=ptr(self.partials))
+
+    def _norm(self) -> float:
+        device_sum(ptr(self.partials), self.levels[0].n_int, ptr(self.sumbuf))
+        return math.sqrt(float(self.sumbuf.item()))
+
+    def iterate(self, u, g=None):
+        """One MGRIT cycle in place; returns the updated iterate (mgrit.py:218-223)."""
+        self._build()
+        ud, uh = to_device(u)
+        gd = None
+        if g is not None:
+            gd, _ = to_device(g)
+        self._cycle(0, ptr(ud), ptr(gd), False, False)
+        if uh is not None:
+            _writeback(uh, ud)
+            return u
+        return ud
+
+    # -------------------------------------------------------------- solve
+    def solve(self, u=None) -> SolveReport:
+        """Run to the halting rule (mgrit.py:251-285); divergence is reported."""
+        self._build()
+        torch = self._torch
+        cfg = self.config
+        if u is None:
+            u = self.initial_state()
+        ud, uh = to_device(u)
+        up = ptr(ud)
+        torch.cuda.synchronize()
+        start = time.perf_counter()
+        self._residual_partials(up, None)
+        norms = [self._norm()]
+        converged = False
+        it = 0
+        while it < cfg.max_iters:
+            self._cycle(0, up, None, False, True)
+            it += 1
+            norms.append(self._norm())
+            if norms[0] > 0 and norms[-1] / norms[0] <= cfg.tol:
+                converged = True
+                break
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - start
+        self.last_iterate = ud
+        if uh is not None:
+            _writeback(uh, ud)
+        rho = norms[-1] / norms[-2] if len(norms) >= 2 and norms[-2] > 0 else 0.0
+        return SolveReport(norms, it, float(rho), converged, wall)
+
+
+def solve(problem: TimeGridProblem, config: MgritConfig, threads: int = 1,
+          initial_iterate=None) -> SolveReport:
+    """Run MGRIT to the halting rule on the GPU (mgrit.py:288-291)."""
+    return MgritSolver(problem, config, threads).solve(initial_iterate)
