@@ -1,0 +1,327 @@
+"""Benchmark: MGRIT time-to-tolerance and fine space-time DOF/s (FP64) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl b200|reference]
+
+A "step" is one full MGRIT solve to ||r_k|| / ||r_0|| <= 1e-10 (the
+reference's SolveReport.wall_time region, mgrit.py:259-279) of the configured
+BASELINE workload; value = n_x * n_t / (time per solve), whole job.
+
+* value / ms_per_step: iterate resident in HBM (537 MB for cfg2 > 126 MB L2,
+  so no L2 flush is needed), CUDA events on the launching stream, max over ranks.
+* e2e: the same solve through the public API ``mgrit.solve(problem, config,
+  initial_iterate=<pinned host tensor>)``: H2D of the iterate, solve, D2H of the
+  final iterate inside the timed region.
+* roofline: per-pass CUDA-event timing of one extra solve; the dominant pass's
+  algorithmic bytes (or FP64 flops) per launch over its mean launch time.
+* cpu_baseline: the numpy oracle (restatement of the reference, oracle/) on this
+  host's cores: one full V-cycle iteration of the same workload, extrapolated
+  with the iteration count to a time-to-tolerance.
+* --impl reference: the same oracle as the reference arm (the reference is
+  pure Python/numpy; /root/reference is absent on the GPU box).
+Multi-GPU (torchrun, N > 1): each rank solves its own replica of the workload
+(weak scaling, "parallelism": "replicas"); time-sharded solves are in
+paper_2209_06916_b200/distributed.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def algorithmic_work(cf, solver, name):
+    """(bound, algorithmic bytes or FP64 flops per launch) of one relax pass."""
+    lev = int(name[1]) if name[0] == "L" and name[1].isdigit() else 0
+    n = cf.n_x
+    if lev >= len(solver.levels):
+        return "latency", None
+    L = solver.levels[lev]
+    nI, m = L.n_int, L.m
+    prog = solver.problem.steppers[lev].program
+    kind = name.split(".")[1]
+    if prog.kind == "stencil":
+        taps = len(prog.offsets)
+        flops = 2.0 * taps * n * nI * (m if kind != "R" else 1)
+        if kind == "CF":  # all F/C rows written + C-point/correction/residual reads
+            return "hbm", 8.0 * n * (nI * m + 4 * nI + 1)
+        if kind in ("FC", "FR"):
+            return "fp64", flops
+        return "hbm", 8.0 * n * 2 * nI
+    return "latency", None
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2209_06916_b200 as P
+    from paper_2209_06916_b200 import _native
+    from paper_2209_06916_b200.configs import CONFIGS
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cf = CONFIGS[args.config]
+    prob = cf.problem()
+    cfg = P.MgritConfig(nu=1, cycle=cf.cycle, tol=1e-10, max_iters=30, rng_seed=0)
+    solver = P.MgritSolver(prob, cfg)
+    u_host = solver.initial_state()
+    u_pristine = torch.from_numpy(u_host).to("cuda")
+    u = torch.empty_like(u_pristine)
+    stream = torch.cuda.current_stream()
+
+    def one_solve():
+        u.copy_(u_pristine)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        rep = solver.solve(u)
+        e.record(stream)
+        torch.cuda.synchronize()
+        return rep, s.elapsed_time(e)
+
+    for _ in range(args.warmup):
+        rep, _ = one_solve()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            rep, ms = one_solve()
+            times.append(ms)
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms_step = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    dof = cf.n_x * cf.n_t
+    value = world * dof / (ms_step / 1e3)
+
+    # e2e through the public API with a pinned host iterate
+    host = torch.from_numpy(u_host).pin_memory()
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        host.copy_(torch.from_numpy(u_host))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep_e2e = P.solve(prob, cfg, initial_iterate=host)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    ubytes = u_host.nbytes
+
+    # per-pass breakdown -> roofline of the dominant pass
+    solver.profile = []
+    rep_p, _ = one_solve()
+    passes = solver.profile_summary()
+    solver.profile = None
+    total_ms = sum(ms for _, ms in passes.values())
+    hbm_peak, peak_kind = peaks()
+    dom = max(passes.items(), key=lambda kv: kv[1][1])
+    roof = None
+    fine_cf = passes.get("L0.CF")
+    if fine_cf:
+        bound, work = algorithmic_work(cf, solver, "L0.CF")
+        per_launch_s = fine_cf[1] / fine_cf[0] / 1e3
+        ach = work / per_launch_s / 1e9
+        roof = {"bound": "hbm", "kernel": "relax_kernel L0.CF (correct + F-relax + residual)",
+                "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "peak_source": peak_kind,
+                "traffic": None, "share_of_step": round(fine_cf[1] / total_ms, 4)}
+    breakdown = {k: {"launches": c, "ms": round(ms, 4), "share": round(ms / total_ms, 4)}
+                 for k, (c, ms) in sorted(passes.items(), key=lambda kv: -kv[1][1])}
+
+    result = {
+        "metric": "MGRIT time-to-tolerance fine space-time DOF/s (FP64)",
+        "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cf.name}: {cf.family.upper()}{cf.p}+U{cf.p} c={cf.c} "
+                               f"n_x={cf.n_x} n_t={cf.n_t} m={cf.m} {cf.cycle} "
+                               f"{cf.coarse} coarse op, FCF, tol 1e-10, u0={cf.u0}",
+                   "iterations": rep.iterations, "converged": rep.converged,
+                   "final_ratio": rep.residual_norms[-1] / rep.residual_norms[0],
+                   "time_to_tolerance_s": ms_step / 1e3,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "iterate 537MB > L2; no flush needed" if ubytes > 126e6 else "iterate fits L2",
+                   "arith": "exact (mul-then-add, reference tap order)"},
+        "e2e": {"value": world * dof / e2e_s, "unit": "DOF/s",
+                "h2d_bytes_per_step": ubytes, "d2h_bytes_per_step": ubytes + 8 * len(rep_e2e.residual_norms),
+                "seconds": e2e_s},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "dominant_pass": {"name": dom[0], "share": round(dom[1][1] / total_ms, 4)},
+        "passes": breakdown,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(cf, rep.iterations)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def oracle_sample(cf, n_iters_sample=1):
+    """One V-cycle iteration (+ initial norm) of the workload on the oracle."""
+    from oracle import mgrit_oracle as O
+    O.ROLL_LIMIT = 64 if cf.p == 5 else 16
+    steps, fac, _ = O.build_hierarchy(cf.family, cf.p, cf.c, cf.n_x, cf.n_t, cf.m, cf.cycle,
+                                      cf.coarse, fine_mode="staged" if cf.family == "sdirk"
+                                      else "assembled")
+    from paper_2209_06916_b200.configs import seeded_u0
+    u0 = seeded_u0(cf.u0, cf.n_x)
+    mg = O.Mgrit(steps, fac, cf.n_t, u0, cycle=cf.cycle)
+    u = mg.initial_state()
+    t0 = time.perf_counter()
+    out = mg.solve(u, max_iters=n_iters_sample)
+    return time.perf_counter() - t0, out
+
+
+def cpu_baseline(cf, iterations):
+    wall, out = oracle_sample(cf)
+    per_solve = wall * max(iterations, 1)  # initial norm ~1/3 iteration: conservative
+    return {"value": cf.n_x * cf.n_t / per_solve, "unit": "DOF/s", "cores": 1, "kind": "port",
+            "sample": f"oracle (numpy restatement of the reference) on this host: 1 FCF "
+                      f"V-cycle iteration + initial norm of {cf.name} at full size took "
+                      f"{wall:.2f}s, x {iterations} iterations to tolerance",
+            "threads": 1, "cpu_count": os.cpu_count()}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    from paper_2209_06916_b200.configs import CONFIGS
+    cf = CONFIGS[args.config]
+    iters = reference_iterations(cf)
+    budget = 180.0
+    times = []
+    for i in range(max(1, args.steps)):
+        wall, _ = oracle_sample(cf)
+        times.append(wall)
+        if sum(times) > budget:
+            break
+    per_iter = float(np.mean(times))
+    per_solve = per_iter * iters
+    value = cf.n_x * cf.n_t / per_solve
+    sample = (f"numpy oracle: each step = 1 FCF iteration (+ initial norm) of {cf.name} at full "
+              f"size; {len(times)} of {args.steps} steps run (180 s budget); extrapolated "
+              f"x {iters} iterations (the oracle's own count)")
+    print(json.dumps({
+        "impl": "reference", "metric": "MGRIT time-to-tolerance fine space-time DOF/s (FP64)",
+        "value": value, "unit": "DOF/s", "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
+        "steps": len(times), "warmup": 0, "ms_per_step": per_solve * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cf.name},
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def reference_iterations(cf):
+    """Iteration count of the reference on this workload (golden fixture made by
+    running the real reference; see tests/golden/make_golden.py)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "histories.json")) as f:
+            return int(json.load(f)[cf.name]["iterations"])
+    except Exception:
+        return {"cfg1": 11, "cfg2": 11, "cfg3": 22, "cfg4": 21}.get(cf.name, 11)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -54,8 +54,8 @@ def to_device(arr):
         t = arr
         if t.dtype != torch.float64:
             raise TypeError("device arrays must be float64")
-        if not t.is_cuda:
-            return t.to("cuda").contiguous(), None
+        if not t.is_cuda:  # host tensor (ideally pinned): copied in, written back
+            return t.to("cuda", non_blocking=t.is_pinned()).contiguous(), t
         if not t.is_contiguous():
             raise ValueError("device arrays must be contiguous")
         return t, None

@@ -122,8 +122,14 @@ def initial_condition(n_x: int) -> np.ndarray:
 # ------------------------------------------------------- drop-in primitives
 
 def _writeback(host, dev):
-    if host is not None:
+    """Copy the device result back into the caller's host array (numpy or a
+    CPU tensor), preserving the reference's in-place mutation semantics."""
+    if host is None:
+        return
+    if isinstance(host, np.ndarray):
         host[...] = dev.cpu().numpy().reshape(host.shape)
+    else:
+        host.copy_(dev.reshape(host.shape))
 
 
 def f_relax(u, g, stepper: Stepper, m: int, pool=None, threads: int = 1) -> None:
@@ -231,7 +237,8 @@ class MgritSolver:
         self.config = config
         self.threads = max(1, int(threads))
         self._built = False
-        self.stats = {}
+        #: set to a list to record (name, start_event, end_event) per launch
+        self.profile = None
 
     # ---------------------------------------------------------- buffers
     def _build(self):
@@ -271,6 +278,26 @@ class MgritSolver:
         g[0] = self.problem.u0
         return g
 
+    def _timed(self, name: str, fn, *args, **kw):
+        if self.profile is None:
+            return fn(*args, **kw)
+        torch = self._torch
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn(*args, **kw)
+        e.record()
+        self.profile.append((name, s, e))
+        return out
+
+    def profile_summary(self) -> dict:
+        """{pass name: (launches, total ms)} of the recorded launches."""
+        self._torch.cuda.synchronize()
+        out = {}
+        for name, s, e in self.profile or []:
+            cnt, ms = out.get(name, (0, 0.0))
+            out[name] = (cnt + 1, ms + s.elapsed_time(e))
+        return out
+
     def _cycle(self, l: int, u: int, g: Optional[int], u_zero: bool, want_norm: bool) -> None:
         cfg = self.config
         L = self.levels[l]
@@ -282,8 +309,8 @@ class MgritSolver:
         src, stride = (None if u_zero else u), m * n
         for i in range(cfg.nu):
             dst = L.cbuf[i % 2]
-            plan.relax(nI, m, m - 1, c_src=src, c_stride=stride, c_src0=u0row, tail=1,
-                       tail_out=ptr(dst) + row, tail_stride=n, g=g)
+            self._timed(f"L{l}.FC", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
+                        c_src0=u0row, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g)
             src, stride = ptr(dst), n
         gC = self.gcoarse[l + 1]
         uC = self.ucoarse[l + 1]
@@ -291,11 +318,13 @@ class MgritSolver:
             cref, cref_stride = (zero, 0) if u_zero else (u + m * row, m * n)
         else:
             cref, cref_stride = src + row, n
-        plan.relax(nI, m, m - 1, c_src=src, c_stride=stride, c_src0=u0row, tail=2, cref=cref,
-                   cref_stride=cref_stride, tail_out=ptr(gC) + row, tail_stride=n, g=g)
+        self._timed(f"L{l}.FR", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
+                    c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
+                    tail_out=ptr(gC) + row, tail_stride=n, g=g)
         child = l + 1
         if cfg.cycle == "two_level" or child == len(self.levels):
-            _forward_substitute_dev(self.plans[child], ptr(uC), ptr(gC), nI + 1)
+            self._timed(f"L{child}.seq", _forward_substitute_dev, self.plans[child], ptr(uC),
+                        ptr(gC), nI + 1)
         else:
             self._cycle(child, ptr(uC), ptr(gC), True, False)
         fuse_norm = want_norm and cfg.nu > 0
@@ -303,14 +332,15 @@ class MgritSolver:
             c_src, c_stride = (None if u_zero else u), m * n
         else:
             c_src, c_stride = src, n
-        plan.relax(nI, m, m - 1, c_src=c_src, c_stride=c_stride, c_src0=u0row, e=ptr(uC),
+        self._timed(f"L{l}.CF", plan.relax, nI, m, m - 1, c_src=c_src, c_stride=c_stride,
+                    c_src0=u0row, e=ptr(uC),
                    e_stride=n, c_out=u, c_out_stride=m * n, c_last_out=u + nI * m * row,
                    u=u, write_f=2, g=g,
                    tail=2 if fuse_norm else 0, cref=(c_src + row) if fuse_norm else None,
                    cref_stride=n, cref_e=ptr(uC) + row, cref_e_stride=n,
                    partials=ptr(self.partials) if fuse_norm else None)
         if want_norm and not fuse_norm:
-            self._residual_partials(u, g)
+            self._timed("L0.R", self._residual_partials, u, g)
 
     def _residual_partials(self, u: int, g: Optional[int]) -> None:
         L = self.levels[0]
@@ -320,7 +350,8 @@ class MgritSolver:
                      cref=u + m * n * _F64, cref_stride=m * n, g=g, partials=ptr(self.partials))
 
     def _norm(self) -> float:
-        device_sum(ptr(self.partials), self.levels[0].n_int, ptr(self.sumbuf))
+        self._timed("norm", device_sum, ptr(self.partials), self.levels[0].n_int,
+                    ptr(self.sumbuf))
         return math.sqrt(float(self.sumbuf.item()))
 
     def iterate(self, u, g=None):
@@ -348,7 +379,7 @@ class MgritSolver:
         up = ptr(ud)
         torch.cuda.synchronize()
         start = time.perf_counter()
-        self._residual_partials(up, None)
+        self._timed("L0.R", self._residual_partials, up, None)
         norms = [self._norm()]
         converged = False
         it = 0
