@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -13,6 +14,7 @@
 #include <tuple>
 #include <vector>
 
+#include "mgb_cluster.cuh"
 #include "mgb_registry.h"
 
 using mgb::Factor;
@@ -50,6 +52,7 @@ void ensure_registered() {
     mgb::register_win_fast();
     mgb::register_gen();
     mgb::register_rk();
+    mgb::register_slgc();
   });
 }
 
@@ -302,16 +305,89 @@ __global__ void sum_kernel(const double* __restrict__ p, long long n, double* ou
 }
 }  // namespace mgb
 
+struct ClusterVariant {
+  int C = 0, P = 0, T = 0, smem = 0, max_clusters = 0;
+  const void* fn = nullptr;
+};
+
 struct mgb_step {
   StepParams hp;
   StepParams* dp = nullptr;
   int dkind = 0, P = 1, T = 1, S = 1, span = 0, nst = 1, exact = 1;
-  int threads = 32, smem = 0, max_grid = 1;
+  int threads = 32, smem = 0, max_grid = 1, sms = 148;
   const void* fn = nullptr;
   double* ws = nullptr;
   long long ws_slot = 0;
   int ws_slots = 0;
+  std::vector<ClusterVariant> clusters;  // SL_GMRES: cluster sizes 16, 8, 4, 2
 };
+
+namespace {
+// Cluster launch variants for SL_GMRES: C CTAs per interval, P <= 2 points per
+// thread, 32 <= T <= 256 threads per CTA, column cap 10 or 20.
+void prepare_clusters(mgb_step* st) {
+  if (st->dkind != mgb::K_SLG) return;
+  const int n = st->hp.n, cap = st->hp.cap;
+  const int capt = cap <= 10 ? 10 : (cap <= 20 ? 20 : 0);
+  if (!capt) return;
+  for (int C : {16, 8, 4, 2}) {
+    if (n % C) continue;
+    const int nc = n / C;
+    int P = 0;
+    for (int p : {2, 1})
+      if (nc % p == 0 && nc / p <= 256 && nc / p >= 32 && (nc / p) % 32 == 0) {
+        P = p;
+        break;
+      }
+    if (!P) continue;
+    // every halo read must come from an adjacent slice
+    bool ok = nc >= 2 * mgb::CL_H;
+    for (int k = 0; k < st->hp.ntap2; ++k) {
+      int o = st->hp.tap2_off[k];
+      o = o > n / 2 ? o - n : o;
+      ok = ok && std::abs(o) <= mgb::CL_H;
+    }
+    if (!ok) continue;
+    const void* fn = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(reg_mutex());
+      auto it = registry().find(std::make_tuple((int)mgb::K_SLGC, P, capt, 1, 1));
+      if (it == registry().end()) continue;
+      fn = it->second;
+    }
+    ClusterVariant v;
+    v.C = C;
+    v.P = P;
+    v.T = nc / P;
+    v.fn = fn;
+    v.smem = (int)(sizeof(StepParams) + 8 * (size_t)(capt == 10 ? mgb::ClLayout<10>::total(nc)
+                                                                  : mgb::ClLayout<20>::total(nc)));
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem) != cudaSuccess) continue;
+    if (C > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(v.T);
+    cfg.dynamicSmemBytes = v.smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = C;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    v.max_clusters = ncl;
+    st->clusters.push_back(v);
+  }
+}
+}  // namespace
 
 extern "C" {
 
@@ -431,6 +507,8 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     return fail(MGB_ERR_UNSUPPORTED, std::string("kernel cannot be resident: ") + cudaGetErrorString(e));
   }
   st->max_grid = nb * sms;
+  st->sms = sms;
+  prepare_clusters(st);
   e = cudaMalloc(&st->dp, sizeof(StepParams));
   if (e != cudaSuccess) { delete st; return fail(MGB_ERR_CUDA, "cudaMalloc params"); }
   e = cudaMemcpy(st->dp, &hp, sizeof(StepParams), cudaMemcpyHostToDevice);
@@ -478,6 +556,30 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   L.ws = nullptr;
   L.ws_slot = 0;
   long long grid = std::min<long long>(a->n_intervals, st->max_grid);
+  static const bool no_cluster = std::getenv("MGB_NO_CLUSTER") != nullptr;
+  if (st->dkind == mgb::K_SLG && !no_cluster) {
+    for (const ClusterVariant& v : st->clusters) {  // largest cluster size that runs in one wave
+      if (a->n_intervals > (long long)v.max_clusters) continue;
+      const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(ncl * v.C));
+      cfg.blockDim = dim3(v.T);
+      cfg.dynamicSmemBytes = v.smem;
+      cfg.stream = (cudaStream_t)stream;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = v.C;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      const StepParams* dpc = st->dp;
+      void* cargs[] = {(void*)&dpc, (void*)&L};
+      CUDA_TRY(cudaLaunchKernelExC(&cfg, v.fn, cargs));
+      g_launches++;
+      return MGB_OK;
+    }
+  }
   if (st->dkind == mgb::K_SLG) {
     int rc = mgb_step_reserve_workspace(st, stream);
     if (rc) return rc;
