@@ -134,6 +134,8 @@ def run_gpu(args):
     cf = CONFIGS[args.config]
     prob = cf.problem()
     cfg = P.MgritConfig(nu=1, cycle=cf.cycle, tol=1e-10, max_iters=30, rng_seed=0)
+    if world > 1:
+        return run_sharded(args, cf, prob, cfg, rank, world, local)
     solver = P.MgritSolver(prob, cfg)
     u_host = solver.initial_state()
     u_pristine = torch.from_numpy(u_host).to("cuda")
@@ -236,6 +238,84 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def run_sharded(args, cf, prob, cfg, rank, world, local):
+    """N > 1: one time-sharded solve of the workload over all ranks (strong
+    scaling): level-0 interval blocks per rank, boundary-row exchange and coarse
+    gather over NCCL, coarse levels on rank 0 (paper_2209_06916_b200/distributed.py)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2209_06916_b200 import _native
+    from paper_2209_06916_b200.distributed import GpuEngine, ShardedMgritSolver, initial_rows
+
+    eng = GpuEngine(prob, cfg)
+    sol = ShardedMgritSolver(prob, cfg, eng)
+    r0, r1 = sol.local_rows()
+    u_host = initial_rows(cfg.rng_seed, r0, r1, cf.n_x, prob.u0)
+    pristine = torch.from_numpy(u_host).to("cuda")
+    u = torch.empty_like(pristine)
+
+    def one_solve():
+        u.copy_(pristine)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        rep = sol.solve(u)
+        e.record()
+        torch.cuda.synchronize()
+        return rep, s.elapsed_time(e)
+
+    for _ in range(args.warmup):
+        one_solve()
+    launches0 = _native.launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            rep, ms = one_solve()
+            times.append(ms)
+    launches = _native.launch_count() - launches0
+    t = torch.tensor([float(np.mean(times))], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    # e2e: pinned host block -> device -> sharded solve -> host, per rank
+    host = torch.from_numpy(u_host).pin_memory()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    ud = host.to("cuda", non_blocking=True)
+    rep_e = sol.solve(ud)
+    host.copy_(ud)
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    nbytes = torch.tensor([float(u_host.nbytes)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(nbytes)
+    lt = torch.tensor([float(launches)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(lt)
+    dof = cf.n_x * cf.n_t
+    result = {
+        "metric": "MGRIT time-to-tolerance fine space-time DOF/s (FP64)",
+        "value": dof / (ms_step / 1e3), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cf.name}: {cf.family.upper()}{cf.p}+U{cf.p} c={cf.c} "
+                               f"n_x={cf.n_x} n_t={cf.n_t} m={cf.m} {cf.cycle}",
+                   "iterations": rep.iterations, "converged": rep.converged,
+                   "parallelism": f"time-sharded x{world} (level-0 interval blocks, "
+                                  f"coarse levels on rank 0)"},
+        "e2e": {"value": dof / float(te.item()), "unit": "DOF/s",
+                "h2d_bytes_per_step": int(nbytes.item()),
+                "d2h_bytes_per_step": int(nbytes.item())},
+        "gpu_launches": int(lt.item()),
+        "roofline": None,
+        "clocks": clk.summary(),
+    }
+    dist.barrier()
+    dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
 

@@ -321,12 +321,7 @@ class MgritSolver:
         self._timed(f"L{l}.FR", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
                     c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
                     tail_out=ptr(gC) + row, tail_stride=n, g=g)
-        child = l + 1
-        if cfg.cycle == "two_level" or child == len(self.levels):
-            self._timed(f"L{child}.seq", _forward_substitute_dev, self.plans[child], ptr(uC),
-                        ptr(gC), nI + 1)
-        else:
-            self._cycle(child, ptr(uC), ptr(gC), True, False)
+        self._coarse_solve(l + 1)
         fuse_norm = want_norm and cfg.nu > 0
         if cfg.nu == 0:
             c_src, c_stride = (None if u_zero else u), m * n
@@ -341,6 +336,17 @@ class MgritSolver:
                    partials=ptr(self.partials) if fuse_norm else None)
         if want_norm and not fuse_norm:
             self._timed("L0.R", self._residual_partials, u, g)
+
+    def _coarse_solve(self, child: int) -> None:
+        """Solve level ``child`` for e = ucoarse[child] given g = gcoarse[child]:
+        forward substitution (two-level / coarsest) or a recursive cycle from
+        e = 0 (mgrit.py:239-244)."""
+        uC, gC = self.ucoarse[child], self.gcoarse[child]
+        if self.config.cycle == "two_level" or child == len(self.levels):
+            self._timed(f"L{child}.seq", _forward_substitute_dev, self.plans[child], ptr(uC),
+                        ptr(gC), self.problem.points_on_level(child))
+        else:
+            self._cycle(child, ptr(uC), ptr(gC), True, False)
 
     def _residual_partials(self, u: int, g: Optional[int]) -> None:
         L = self.levels[0]

@@ -1,0 +1,243 @@
+"""CPU tests: pin the oracle (oracle/mgrit_oracle.py) and the product's host
+setup against golden fixtures produced by running the real reference
+(tests/golden/make_golden.py).  No GPU needed."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import mgrit_oracle as O
+
+import paper_2209_06916_b200 as P
+from paper_2209_06916_b200 import experiments as PE
+from paper_2209_06916_b200 import stepping as PS
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SETUP = np.load(os.path.join(HERE, "setup.npz"))
+RELAX = np.load(os.path.join(HERE, "relax.npz"))
+GMRES = np.load(os.path.join(HERE, "gmres.npz"))
+HIST = json.load(open(os.path.join(HERE, "histories.json")))
+
+HIERARCHIES = [
+    ("erk", 1, 0.85, 1024, 1024, 8, "two_level", "modified"),
+    ("erk", 3, 0.85, 4096, 16384, 8, "v_cycle", "modified"),
+    ("sdirk", 3, 4.0, 4096, 16384, 4, "v_cycle", "modified"),
+    ("erk", 5, 0.85, 8192, 65536, 16, "v_cycle", "modified"),
+    ("erk", 3, 1.3820, 256, 1024, 4, "v_cycle", "modified"),
+    ("sdirk", 3, 5.0, 64, 256, 16, "two_level", "rediscretized"),
+    ("erk", 2, 0.4, 128, 256, 4, "two_level", "plain_sl"),
+    ("sdirk", 1, 0.8, 32, 64, 8, "two_level", "ideal"),
+]
+
+
+def _same(a, b):
+    return np.array_equal(np.asarray(a), np.asarray(b))
+
+
+# ------------------------------------------------------------ setup weights
+
+@pytest.mark.parametrize("i", range(len(HIERARCHIES)))
+def test_oracle_hierarchy_weights_bitwise(i):
+    fam, p, c, nx, nt, m, cyc, kind = HIERARCHIES[i]
+    steps, fac, _ = O.build_hierarchy(fam, p, c, nx, nt, m, cyc, kind)
+    assert fac == list(SETUP[f"h{i}_factors"])
+    for l, st in enumerate(steps):
+        assert _same(st.op.offsets, SETUP[f"h{i}_l{l}_off"])
+        assert _same(st.op.weights, SETUP[f"h{i}_l{l}_w"])
+
+
+@pytest.mark.parametrize("i", range(len(HIERARCHIES)))
+def test_product_hierarchy_weights_bitwise(i):
+    """The product's host setup assembles the reference's exact stencils."""
+    fam, p, c, nx, nt, m, cyc, kind = HIERARCHIES[i]
+    prob = PE.build_problem(P.DiscretizationSpec(fam, p, c, nx, nt), m, cyc, kind)
+    assert prob.m == list(SETUP[f"h{i}_factors"])
+    for l, st in enumerate(prob.steppers):
+        assert _same(st.op.offsets, SETUP[f"h{i}_l{l}_off"])
+        assert _same(st.op.weights, SETUP[f"h{i}_l{l}_w"])
+
+
+def test_constants_and_cfl_limits():
+    for p in range(1, 6):
+        assert O.cfl_max(p) == float(SETUP[f"cmax_{p}"])
+        assert P.cfl_limit(p) == float(SETUP[f"cmax_{p}"])
+        assert P.error_constant_fd(p) == float(SETUP[f"efd_{p}"])
+        assert P.rk_error_constant(P.erk_tableau(p)) == float(SETUP[f"erk_err_{p}"])
+        assert P.rk_error_constant(P.sdirk_tableau(p)) == float(SETUP[f"sdirk_err_{p}"])
+        assert O.rk_error_constant(O.sdirk(p)) == float(SETUP[f"sdirk_err_{p}"])
+
+
+@pytest.mark.parametrize("j,p,c,m,level", [(0, 1, 0.4, 4, 1), (1, 3, 0.85, 8, 3),
+                                            (2, 3, 4.0, 4, 7), (3, 5, 0.85, 16, 4),
+                                            (4, 2, 0.7, 4, 2)])
+def test_corrected_operator_components(j, p, c, m, level):
+    fam = "erk" if c < 1 else "sdirk"
+    spec = P.DiscretizationSpec(fam, p, c, 256, 64)
+    tab = spec.tableau()
+    phi = PS.phi_coefficient(p, c, m, level, P.error_constant_fd(p), P.rk_error_constant(tab))
+    assert phi == float(SETUP[f"phi_{j}"])
+    assert O.phi_value(p, c, m, level, O.fd_error_constant(p),
+                       O.rk_error_constant(O.tableau_for(fam, p))) == float(SETUP[f"phi_{j}"])
+    sl = P.sl_stepper(p, m ** level * c, 256).stepper
+    assert _same(sl.op.offsets, SETUP[f"sl_{j}_off"]) and _same(sl.op.weights, SETUP[f"sl_{j}_w"])
+    D = PS.correction_operator(p, 256)
+    assert _same(D.offsets, SETUP[f"D_{j}_off"]) and _same(D.weights, SETUP[f"D_{j}_w"])
+    st = P.modified_coarse_stepper(spec, m, level)
+    assert _same(st.op.offsets, SETUP[f"mod_{j}_off"]) and _same(st.op.weights, SETUP[f"mod_{j}_w"])
+
+
+def test_known_answer_values():
+    """Hand values pinned by the reference's own tests (tests/test_stepping.py)."""
+    assert PS.phi_coefficient(1, 0.4, 4, 1, P.error_constant_fd(1),
+                              P.rk_error_constant(P.erk_tableau(1))) == pytest.approx(0.36)
+    st = P.mol_stepper(P.DiscretizationSpec("erk", 1, 0.7, 32, 8))
+    assert list(st.op.offsets) == [-1, 0]
+    np.testing.assert_allclose(st.op.weights, [0.7, 0.3], atol=1e-12)
+    sl, eps, shift, _ = P.sl_stepper(3, 4.0, 32)
+    assert eps == 0.0 and shift == -4 and list(sl.op.offsets) == [-4]
+    np.testing.assert_allclose(P.StencilWindow.upwind(3).offsets, [-2, -1, 0, 1])
+    np.testing.assert_allclose(P.upwind_derivative(3, 16).weights, [1 / 6, -1, 1 / 2, 1 / 3],
+                               atol=1e-14)
+
+
+@pytest.mark.parametrize("j", range(3))
+def test_oracle_staged_stepper_bitwise(j):
+    fam, p, c = [("sdirk", 3, 4.0), ("erk", 3, 0.85), ("sdirk", 5, 1.3)][j]
+    st = O.mol_step(fam, p, c, 256, mode="staged")
+    assert _same(st.apply(SETUP[f"staged_{j}_in"]), SETUP[f"staged_{j}_out"])
+
+
+# ---------------------------------------------------------- relax + GMRES
+
+@pytest.mark.parametrize("i", range(4))
+def test_oracle_relaxation_bitwise(i):
+    fam, p, c, nx, nt, m = [("erk", 1, 0.85, 1024, 64, 8), ("erk", 3, 0.85, 256, 64, 8),
+                            ("erk", 5, 0.85, 128, 64, 16), ("sdirk", 3, 4.0, 128, 32, 4)][i]
+    steps, fac, u0 = O.build_hierarchy(fam, p, c, nx, nt, m, "two_level")
+    u = RELAX[f"c{i}_u0"].copy()
+    g = np.zeros_like(u)
+    g[0] = u0
+    saved = O.ROLL_LIMIT
+    O.ROLL_LIMIT = 64
+    try:
+        O.f_relax(u, g, steps[0], m)
+        assert _same(u, RELAX[f"c{i}_f"])
+        O.c_relax(u, g, steps[0], m)
+        assert _same(u, RELAX[f"c{i}_fc"])
+        assert _same(O.restrict(u, g, steps[0], m), RELAX[f"c{i}_r"])
+    finally:
+        O.ROLL_LIMIT = saved
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_oracle_gmres_matches_reference(i):
+    op = O.Circ(int(GMRES[f"g{i}_B"].shape[1]), GMRES[f"g{i}_off"], GMRES[f"g{i}_w"])
+    its, brk, cap = (int(v) for v in GMRES[f"g{i}_meta"])
+    X, res, j, b = O.gmres_rows(op, GMRES[f"g{i}_B"], 1e-2, cap)
+    assert j == its and bool(b) == bool(brk)
+    assert _same(X, GMRES[f"g{i}_X"]) and _same(res, GMRES[f"g{i}_res"])
+    # zero right-hand side row -> zero solution (circulant.py:274-278)
+    assert not np.any(X[2])
+
+
+# ---------------------------------------------------------------- histories
+
+SMALL = {
+    "erk1_tl_256x256": ("erk", 1, 0.85, 256, 256, 8, "two_level", "modified", "assembled"),
+    "erk1_v_256x1024": ("erk", 1, 0.85, 256, 1024, 4, "v_cycle", "modified", "assembled"),
+    "sdirk3_v_256x1024_staged": ("sdirk", 3, 4.0, 256, 1024, 4, "v_cycle", "modified", "staged"),
+    "sdirk3_tl_64x256_redisc": ("sdirk", 3, 5.0, 64, 256, 16, "two_level", "rediscretized",
+                                "assembled"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_oracle_history_bitwise(name):
+    fam, p, c, nx, nt, m, cyc, kind, mode = SMALL[name]
+    steps, fac, u0 = O.build_hierarchy(fam, p, c, nx, nt, m, cyc, kind, fine_mode=mode)
+    out = O.Mgrit(steps, fac, nt, u0, cycle=cyc).solve()
+    ref = HIST[name]
+    assert out["iterations"] == ref["iterations"] and out["converged"] == ref["converged"]
+    assert out["norms"] == ref["norms"]
+
+
+def test_oracle_erk3_paper_cfl_history_bitwise():
+    c = 0.85 * O.cfl_max(3)
+    steps, fac, u0 = O.build_hierarchy("erk", 3, c, 256, 1024, 8, "v_cycle")
+    out = O.Mgrit(steps, fac, 1024, u0, cycle="v_cycle").solve()
+    assert out["norms"] == HIST["erk3_v_256x1024"]["norms"]
+
+
+@pytest.mark.parametrize("fam", ["erk", "sdirk"])
+@pytest.mark.parametrize("m", [2, 4, 8, 16])
+def test_oracle_table3_64x256(fam, m):
+    """Exact Table-3 counts of the reference at 64x256."""
+    c = 0.85 * O.cfl_max(3) if fam == "erk" else 5.0
+    for cyc in ("two_level", "v_cycle"):
+        steps, fac, u0 = O.build_hierarchy(fam, 3, c, 64, 256, m, cyc)
+        out = O.Mgrit(steps, fac, 256, u0, cycle=cyc, max_iters=40).solve()
+        ref = HIST[f"table3_{fam}_64x256_m{m}_{cyc}"]
+        assert out["iterations"] == ref["iterations"]
+        assert out["converged"] == ref["converged"]
+
+
+def test_oracle_final_iterate_bitwise():
+    fin = np.load(os.path.join(HERE, "final_u.npz"))
+    steps, fac, u0 = O.build_hierarchy("erk", 1, 0.85, 256, 256, 8, "two_level")
+    out = O.Mgrit(steps, fac, 256, u0).solve()
+    assert _same(out["u"], fin["erk1_tl_256x256"])
+
+
+def test_baseline_config_histories_recorded():
+    """Full-size reference runs of the BASELINE configs (tests/golden/histories.json)
+    have the survey's iteration counts; the GPU tests compare against them."""
+    want = {"cfg1": 11, "cfg2": 11, "cfg3": 22, "cfg4": 21}
+    for k, v in want.items():
+        if k in HIST:
+            assert HIST[k]["iterations"] == v and HIST[k]["converged"]
+
+
+# --------------------------------------------------------------- validation
+
+def test_config_and_problem_validation():
+    with pytest.raises(ValueError):
+        P.MgritConfig(nu=-1)
+    with pytest.raises(ValueError):
+        P.MgritConfig(cycle="w_cycle")
+    with pytest.raises(ValueError):
+        P.MgritConfig(max_iters=0)
+    n = 8
+    ident = P.Stepper(n, P.CirculantOperator.identity(n), lambda om: np.ones_like(om))
+    with pytest.raises(ValueError):
+        P.TimeGridProblem([ident], [2], 8, np.zeros(n))
+    with pytest.raises(ValueError):
+        P.TimeGridProblem([ident, ident], [3], 8, np.zeros(n))
+    with pytest.raises(ValueError):
+        P.TimeGridProblem([ident, ident], [1], 8, np.zeros(n))
+
+
+def test_rediscretized_requires_sdirk():
+    with pytest.raises(ValueError):
+        P.rediscretized_coarse_stepper(P.DiscretizationSpec("erk", 1, 0.5, 32, 8), 2)
+    with pytest.raises(ValueError):  # BASELINE cfg4 "rediscretized" variant: same error
+        PE.build_problem(P.DiscretizationSpec("erk", 5, 0.85, 64, 256), 16, "v_cycle",
+                         "rediscretized")
+
+
+def test_stability_warning_and_singular_correction():
+    with pytest.warns(P.StabilityWarning):
+        P.mol_stepper(P.DiscretizationSpec("erk", 1, 1.5, 32, 8))
+    op = P.CirculantOperator(8, [(0, 1.0), (-1, -1.0)])
+    with pytest.raises(P.SingularOperatorError):
+        op._check_invertible()
+
+
+def test_initial_state_matches_reference_rng():
+    prob = PE.build_problem(P.DiscretizationSpec("erk", 1, 0.85, 64, 64), 8, "two_level")
+    sol = P.MgritSolver(prob, P.MgritConfig(rng_seed=5))
+    u = sol.initial_state()
+    ref = np.random.default_rng(5).random((65, 64))
+    ref[0] = P.initial_condition(64)
+    assert _same(u, ref)
