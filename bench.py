@@ -18,9 +18,10 @@ BASELINE workload; value = n_x * n_t / (time per solve), whole job.
   with the iteration count to a time-to-tolerance.
 * --impl reference: the same oracle as the reference arm (the reference is
   pure Python/numpy; /root/reference is absent on the GPU box).
-Multi-GPU (torchrun, N > 1): each rank solves its own replica of the workload
-(weak scaling, "parallelism": "replicas"); time-sharded solves are in
-paper_2209_06916_b200/distributed.py.
+Multi-GPU (torchrun, N > 1): ONE time-sharded solve of the workload over the N
+ranks (strong scaling): level-0 interval blocks per rank, boundary C-point rows
+and the coarse right-hand side exchanged over NCCL, coarse levels on rank 0
+(paper_2209_06916_b200/distributed.py).
 """
 
 from __future__ import annotations
@@ -110,8 +111,8 @@ def algorithmic_work(cf, solver, name):
     if prog.kind == "stencil":
         taps = len(prog.offsets)
         flops = 2.0 * taps * n * nI * (m if kind != "R" else 1)
-        if kind == "CF":  # all F/C rows written + C-point/correction/residual reads
-            return "hbm", 8.0 * n * (nI * m + 4 * nI + 1)
+        if kind == "CF":  # all F/C rows written once + C-point and correction rows read once
+            return "hbm", 8.0 * n * (nI * m + 1 + 2 * (nI + 1))
         if kind in ("FC", "FR"):
             return "fp64", flops
         return "hbm", 8.0 * n * 2 * nI

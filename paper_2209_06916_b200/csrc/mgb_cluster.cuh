@@ -134,11 +134,11 @@ __device__ __forceinline__ void cl_sum_b(ClCtx& c, double (&v)[N], int cnt) {
   const int p = c.parity;
   double* cred = c.cred + p * (CL_MAXC * N);
   const uint32_t lcred = smem_u32(cred);
-  for (int idx = c.t; idx < cnt * c.C; idx += blockDim.x) {
-    const int i = idx % cnt, r = idx / cnt;
+  if (c.t < cnt) {  // cnt <= N <= 32 <= blockDim: thread i owns value i
     double s = 0.0;
-    for (int w = 0; w < c.nw; ++w) s += c.wred[w * N + i];
-    st_cluster_f64(cl_map(lcred + 8u * (c.rank * N + i), r), s);
+    for (int w = 0; w < c.nw; ++w) s += c.wred[w * N + c.t];
+    const uint32_t src = lcred + 8u * (c.rank * N + c.t);
+    for (int r = 0; r < c.C; ++r) st_cluster_f64(cl_map(src, r), s);
   }
   cluster_barrier();  // peers' partials (and any halo stores) now visible
   if (cnt <= 4) {  // every thread sums the few columns itself (no extra barrier)
@@ -363,18 +363,20 @@ __device__ void cl_gmres(ClCtx& c, double* sm, const double (&b)[P],
       for (int q = 0; q < P; ++q) Zs[(j + 1) * c.nc + l0 + q] = aw[q] * inv;
     }
     if (c.t == 0) {  // Givens on column j (identical in every CTA)
-      hcol[j + 1] = hn;
+      // the rotated entry is carried in a register; cs/sn/h loads are off the chain
+      double hi = hcol[0];
+#pragma unroll 4
       for (int i = 0; i < j; ++i) {
-        const double hi = hcol[i], hi1 = hcol[i + 1];
-        hcol[i] = __dadd_rn(__dmul_rn(cs[i], hi), __dmul_rn(sn[i], hi1));
-        hcol[i + 1] = __dadd_rn(__dmul_rn(-sn[i], hi), __dmul_rn(cs[i], hi1));
+        const double ci = cs[i], si = sn[i], hi1 = hcol[i + 1];
+        hcol[i] = __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1));
+        hi = __dadd_rn(__dmul_rn(-si, hi), __dmul_rn(ci, hi1));
       }
-      double den = hypot(hcol[j], hcol[j + 1]);
+      double den = hypot(hi, hn);
       den = den > 0.0 ? den : 1.0;
-      const double cj = hcol[j] / den, sj = hcol[j + 1] / den;
+      const double cj = hi / den, sj = hn / den;
       cs[j] = cj;
       sn[j] = sj;
-      hcol[j] = __dadd_rn(__dmul_rn(cj, hcol[j]), __dmul_rn(sj, hcol[j + 1]));
+      hcol[j] = __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn));
       const double gj = gg[j];
       gg[j + 1] = __dmul_rn(-sj, gj);
       gg[j] = __dmul_rn(cj, gj);

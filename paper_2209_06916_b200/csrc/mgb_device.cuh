@@ -48,6 +48,7 @@ struct StepParams {
   int kind, n, P, T, S, exact, repeat, stages;
   int implicit, nfac, shift, cap;
   int ntap, ntap2, win_lo, win_span;
+  int win2_lo, win2_span, win2_ok, pad2_;  // contiguous implicit stencil (GMRES operator)
   double gain_inv, tol;
   double A[MAX_ST * MAX_ST], b[MAX_ST];
   int tap_off[MAX_TAPS];
@@ -55,6 +56,7 @@ struct StepParams {
   int tap2_off[MAX_TAPS2];
   double tap2_w[MAX_TAPS2];
   double win_w[32];
+  double win2_w[8];
   Factor fac[MAX_FAC];
 };
 static_assert(sizeof(StepParams) % 16 == 0, "StepParams must be 16-byte sized");
@@ -135,8 +137,9 @@ struct Ctx {
   int parity;
 };
 
-// Deterministic block reduction: warp butterfly, then every thread sums the
-// warp partials in warp order -> bitwise identical result in all threads.
+// Deterministic block reduction: warp butterfly, one CTA barrier, then every
+// warp butterflies the warp partials (lane i holds partial i) -> the same
+// summation tree in every warp, bitwise identical result in all threads.
 __device__ __forceinline__ double block_sum(Ctx& c, double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -145,8 +148,10 @@ __device__ __forceinline__ double block_sum(Ctx& c, double v) {
   if (lane == 0) slot[w] = v;
   __syncthreads();
   const int nw = blockDim.x >> 5;
-  double s = 0.0;
-  for (int i = 0; i < nw; ++i) s += slot[i];
+  double s = lane < nw ? slot[lane] : 0.0;
+  for (int o = 16; o > 0; o >>= 1)
+    if (o < nw) s += __shfl_xor_sync(0xffffffffu, s, o);  // lanes >= nw hold 0
+  s = __shfl_sync(0xffffffffu, s, 0);
   c.parity ^= 1;
   return s;
 }
@@ -325,10 +330,77 @@ __device__ void chain_solve(Ctx& c, double (&x)[P]) {
 
 // ------------------------------------------------------------------ GMRES
 
+// Krylov basis element (t, q) of vector i: pairs (q, q+1) are stored as one
+// 16-byte word at ((q/2) * T + t) * 2 so every warp load is a coalesced LDG.128.
+template <int P>
+__device__ __forceinline__ void vec_load(const double* __restrict__ Vi, int t, int T, double (&x)[P]) {
+  if constexpr (P % 2 == 0) {
+    const double2* v2 = reinterpret_cast<const double2*>(Vi);
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      const double2 d = v2[q * T + t];
+      x[2 * q] = d.x;
+      x[2 * q + 1] = d.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] = Vi[q * T + t];
+  }
+}
+template <int P>
+__device__ __forceinline__ void vec_store(double* Vi, int t, int T, const double (&x)[P]) {
+  if constexpr (P % 2 == 0) {
+    double2* v2 = reinterpret_cast<double2*>(Vi);
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) v2[q * T + t] = make_double2(x[2 * q], x[2 * q + 1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < P; ++q) Vi[q * T + t] = x[q];
+  }
+}
+
+// (I - phi D) applied to the resident row: contiguous taps (span <= 6) through
+// a register window, else generic taps.  Exact mode, canonical tap order.
+template <int P>
+__device__ __forceinline__ void apply_op2(const Ctx& c, double (&y)[P]) {
+  const StepParams& sp = *c.sp;
+  if (!sp.win2_ok) {
+    stencil_gen<P, true>(c, sp.ntap2, sp.tap2_off, sp.tap2_w, y);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < P; ++q) y[q] = 0.0;
+  if (!c.own) return;
+  const int lo = sp.win2_lo;
+  int tb = c.t + lo / P;
+  tb = tb >= c.T ? tb - c.T : tb;
+  const int r0 = lo & (P - 1);
+  double win[P + 6];
+#pragma unroll
+  for (int w = 0; w < P + 6; ++w) {
+    const int cw = r0 + w;
+    int tt = tb + cw / P;
+    tt = tt >= c.T ? tt - c.T : tt;
+    tt = tt >= c.T ? tt - c.T : tt;
+    win[w] = c.row[(cw & (P - 1)) * c.S + tt];
+  }
+  const int span = sp.win2_span;
+#pragma unroll
+  for (int k = 0; k <= 6; ++k) {
+    if (k <= span) {
+      const double wk = sp.win2_w[k];
+#pragma unroll
+      for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], __dmul_rn(wk, win[q + k]));
+    }
+  }
+}
+
 // Unrestarted GMRES(x0 = 0) on the circulant (taps2) for the CTA's row,
 // following circulant.py:262-332: MGS Arnoldi, Givens QR, stop when
 // res <= tol or ||h|| <= 1e-14 beta, back substitution, x = V y.
-// V lives in this CTA's HBM/L2 workspace slot, element (t, q) at q*T + t.
+// V lives in this CTA's HBM/L2 workspace slot (coalesced 16-byte layout, next
+// vector prefetched); Givens/g/cs/sn on thread 0 with the rotated entry in a
+// register; normalisations multiply by the reciprocal.
 template <int P>
 __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& depth_out,
                             double& res_out) {
@@ -337,11 +409,11 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   const int cap = sp.cap;
   double* V = c.ws;
   double* R = V + (size_t)(cap + 1) * n;
-  double* cs = R + (size_t)cap * cap;
-  double* sn = cs + cap;
-  double* gg = sn + cap;
   double* hcol = c.gm;
-  double* ybuf = c.gm + MAX_CAP + 2;
+  double* ybuf = hcol + MAX_CAP + 2;
+  double* cs = ybuf + MAX_CAP;
+  double* sn = cs + MAX_CAP;
+  double* gg = sn + MAX_CAP;
 
   double part = 0.0;
   if (c.own) {
@@ -349,20 +421,18 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
     for (int q = 0; q < P; ++q) part = fma(b[q], b[q], part);
   }
   const double beta = sqrt(block_sum(c, part));
-#pragma unroll
-  for (int q = 0; q < P; ++q) x[q] = 0.0;
   if (beta == 0.0) {  // zero right-hand side: x = 0, converged (circulant.py:274-278)
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] = 0.0;
     depth_out = 0;
     res_out = 0.0;
     return;
   }
   double v[P];
+  const double ib = 1.0 / beta;
 #pragma unroll
-  for (int q = 0; q < P; ++q) v[q] = b[q] / beta;
-  if (c.own) {
-#pragma unroll
-    for (int q = 0; q < P; ++q) V[q * T + t] = v[q];
-  }
+  for (int q = 0; q < P; ++q) v[q] = b[q] * ib;
+  if (c.own) vec_store<P>(V, t, T, v);
   if (t == 0) gg[0] = beta;
   double res = 1.0;
   int depth = 0;
@@ -371,64 +441,58 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
     if (c.own) chunk_to_row<P>(c.row, t, c.S, v);
     __syncthreads();
     double w[P];
-    stencil_gen<P, true>(c, sp.ntap2, sp.tap2_off, sp.tap2_w, w);
+    apply_op2<P>(c, w);
     // modified Gram-Schmidt (next basis vector prefetched from L2)
     double vn[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) vn[q] = 0.0;
-    if (c.own && j > 0) {
-#pragma unroll
-      for (int q = 0; q < P; ++q) vn[q] = V[q * T + t];
-    }
+    if (c.own && j > 0) vec_load<P>(V, t, T, vn);
     for (int i = 0; i <= j; ++i) {
-      double vi[P];
+      double vi[P];  // v_j itself is re-read from the resident row (keeps v dead here)
 #pragma unroll
-      for (int q = 0; q < P; ++q) vi[q] = (i == j) ? v[q] : vn[q];
-      if (c.own && i + 1 < j) {
-        const double* Vn = V + (size_t)(i + 1) * n;
-#pragma unroll
-        for (int q = 0; q < P; ++q) vn[q] = Vn[q * T + t];
-      }
-      double p = 0.0;
+      for (int q = 0; q < P; ++q) vi[q] = (i == j) ? (c.own ? c.row[q * c.S + t] : 0.0) : vn[q];
+      if (c.own && i + 1 < j) vec_load<P>(V + (size_t)(i + 1) * n, t, T, vn);
+      double p0 = 0.0, p1 = 0.0;
       if (c.own) {
 #pragma unroll
-        for (int q = 0; q < P; ++q) p = fma(w[q], vi[q], p);
+        for (int q = 0; q < P; q += 2) {
+          p0 = fma(w[q], vi[q], p0);
+          if (q + 1 < P) p1 = fma(w[q + 1], vi[q + 1], p1);
+        }
       }
-      const double h = block_sum(c, p);
+      const double h = block_sum(c, p0 + p1);
       if (t == 0) hcol[i] = h;
 #pragma unroll
       for (int q = 0; q < P; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(h, vi[q]));
     }
-    part = 0.0;
+    double n0 = 0.0, n1 = 0.0;
     if (c.own) {
 #pragma unroll
-      for (int q = 0; q < P; ++q) part = fma(w[q], w[q], part);
-    }
-    const double hn = sqrt(block_sum(c, part));
-    const bool happy = hn <= 1e-14 * beta;
-    const double safe = hn > 0.0 ? hn : 1.0;
-#pragma unroll
-    for (int q = 0; q < P; ++q) v[q] = w[q] / safe;
-    if (c.own) {
-      double* Vj = V + (size_t)(j + 1) * n;
-#pragma unroll
-      for (int q = 0; q < P; ++q) Vj[q * T + t] = v[q];
-    }
-    if (t == 0) {
-      hcol[j + 1] = hn;
-      for (int i = 0; i < j; ++i) {  // stored rotations (circulant.py:308-312)
-        const double hi = hcol[i], hi1 = hcol[i + 1];
-        const double tt = __dadd_rn(__dmul_rn(cs[i], hi), __dmul_rn(sn[i], hi1));
-        hcol[i + 1] = __dadd_rn(__dmul_rn(-sn[i], hi), __dmul_rn(cs[i], hi1));
-        hcol[i] = tt;
+      for (int q = 0; q < P; q += 2) {
+        n0 = fma(w[q], w[q], n0);
+        if (q + 1 < P) n1 = fma(w[q + 1], w[q + 1], n1);
       }
-      double den = hypot(hcol[j], hcol[j + 1]);
+    }
+    const double hn = sqrt(block_sum(c, n0 + n1));
+    const bool happy = hn <= 1e-14 * beta;
+    const double inv = 1.0 / (hn > 0.0 ? hn : 1.0);
+#pragma unroll
+    for (int q = 0; q < P; ++q) v[q] = w[q] * inv;
+    if (c.own) vec_store<P>(V + (size_t)(j + 1) * n, t, T, v);
+    if (t == 0) {  // Givens (circulant.py:308-319), rotated entry carried in a register
+      double hi = hcol[0];
+#pragma unroll 4
+      for (int i = 0; i < j; ++i) {
+        const double ci = cs[i], si = sn[i], hi1 = hcol[i + 1];
+        hcol[i] = __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1));
+        hi = __dadd_rn(__dmul_rn(-si, hi), __dmul_rn(ci, hi1));
+      }
+      double den = hypot(hi, hn);
       den = den > 0.0 ? den : 1.0;
-      const double cj = hcol[j] / den, sj = hcol[j + 1] / den;
+      const double cj = hi / den, sj = hn / den;
       cs[j] = cj;
       sn[j] = sj;
-      hcol[j] = __dadd_rn(__dmul_rn(cj, hcol[j]), __dmul_rn(sj, hcol[j + 1]));
-      hcol[j + 1] = 0.0;
+      hcol[j] = __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn));
       const double gj = gg[j];
       gg[j + 1] = __dmul_rn(-sj, gj);
       gg[j] = __dmul_rn(cj, gj);
@@ -453,12 +517,15 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
     }
   }
   __syncthreads();
+#pragma unroll
+  for (int q = 0; q < P; ++q) x[q] = 0.0;
   if (c.own) {
+    double vi[P];
     for (int i = 0; i < depth; ++i) {
       const double yi = ybuf[i];
-      const double* Vi = V + (size_t)i * n;
+      vec_load<P>(V + (size_t)i * n, t, T, vi);
 #pragma unroll
-      for (int q = 0; q < P; ++q) x[q] = __dadd_rn(x[q], __dmul_rn(yi, Vi[q * T + t]));
+      for (int q = 0; q < P; ++q) x[q] = __dadd_rn(x[q], __dmul_rn(yi, vi[q]));
     }
   }
   depth_out = depth;

@@ -475,6 +475,17 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
       hp.tap2_off[k] = (int)mod_n(d->offsets2[k], n);
       hp.tap2_w[k] = d->weights2[k];
     }
+    {  // register-window form of the (I - phi D) stencil: contiguous, span <= 6
+      bool inc = true;
+      for (int k = 1; k < d->n_taps2; ++k) inc = inc && d->offsets2[k] > d->offsets2[k - 1];
+      const long long sp2 = d->offsets2[d->n_taps2 - 1] - d->offsets2[0];
+      if (inc && sp2 <= 6) {
+        hp.win2_ok = 1;
+        hp.win2_lo = (int)mod_n(d->offsets2[0], n);
+        hp.win2_span = (int)sp2;
+        for (int k = 0; k < d->n_taps2; ++k) hp.win2_w[d->offsets2[k] - d->offsets2[0]] = d->weights2[k];
+      }
+    }
     hp.tol = d->gmres_tol;
     hp.cap = std::min((int)d->gmres_cap, n);
     if (hp.cap < 1 || hp.cap > mgb::MAX_CAP) { delete st; return fail(MGB_ERR_UNSUPPORTED, "GMRES cap must be 1..128"); }
@@ -488,7 +499,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->threads = ((T + 31) / 32) * 32;
   size_t dbl = (size_t)P * S + 64 + 8;
   if (dk == mgb::K_RK || dk == mgb::K_SLD) dbl += 4 * (size_t)T;
-  if (dk == mgb::K_SLG) dbl += 2 * mgb::MAX_CAP + 2;
+  if (dk == mgb::K_SLG) dbl += 5 * mgb::MAX_CAP + 4;  // hcol, y, cs, sn, g
   st->smem = (int)(sizeof(StepParams) + 8 * dbl);
   {
     std::lock_guard<std::mutex> lk(reg_mutex());

@@ -278,3 +278,28 @@ def test_baseline_config_against_reference_history(name):
     r0 = ref["norms"][0]
     dev = max(abs(a - b) / r0 for a, b in zip(rep.residual_norms, ref["norms"]))
     assert dev <= _TOL[name], dev
+
+
+def test_time_sharded_engine_single_rank_matches_solver():
+    """The NCCL time-sharded driver (GpuEngine) on one rank reproduces the
+    single-GPU solver bit for bit (multi-rank logic: tests/test_distributed_gloo.py)."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2209_06916_b200.distributed import GpuEngine, ShardedMgritSolver
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        spec = P.DiscretizationSpec("erk", 3, 0.85, 256, 1024)
+        prob = P.experiments.build_problem(spec, 8, "v_cycle")
+        cfg = P.MgritConfig(cycle="v_cycle")
+        u = O.initial_iterate(0, 1024, 256, prob.u0)
+        ref_u = u.copy()
+        ref = P.solve(prob, cfg, initial_iterate=ref_u)
+        ud = torch.from_numpy(u).cuda()
+        rep = ShardedMgritSolver(prob, cfg, GpuEngine(prob, cfg)).solve(ud)
+        assert rep.iterations == ref.iterations
+        assert np.array_equal(ud.cpu().numpy(), ref_u)
+        np.testing.assert_allclose(rep.residual_norms, ref.residual_norms, rtol=1e-14)
+    finally:
+        dist.destroy_process_group()
