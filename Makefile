@@ -22,3 +22,12 @@ clean:
 	rm -rf build $(OUT)/libmgrit_b200.so
 
 .PHONY: all clean
+
+# phase-timer build of the cluster kernel (tools/cluster_trace.py; not shipped)
+TRACE_BUILD := build/trace
+$(TRACE_BUILD)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(TRACE_BUILD)
+	$(NVCC) $(NVFLAGS) -DMGB_CL_TRACE -c $< -o $@ > $(TRACE_BUILD)/$*.log 2>&1 || (cat $(TRACE_BUILD)/$*.log; exit 1)
+trace: $(patsubst $(BUILD)/%,$(TRACE_BUILD)/%,$(OBJS))
+	$(NVCC) $(ARCH) -shared -o $(OUT)/libmgrit_b200_trace.so $^
+.PHONY: trace

@@ -13,7 +13,8 @@ from typing import Optional
 
 from .errors import DimensionMismatchError, SingularOperatorError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmgrit_b200.so")
+_LIB_NAME = "libmgrit_b200_trace.so" if os.environ.get("MGB_TRACE") else "libmgrit_b200.so"
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", _LIB_NAME)
 
 MGB_OK, MGB_ERR_INVALID, MGB_ERR_DIMENSION, MGB_ERR_SINGULAR, MGB_ERR_CUDA, MGB_ERR_UNSUPPORTED = range(6)
 MGB_STEP_STENCIL, MGB_STEP_RK_STAGED, MGB_STEP_SL_DIRECT, MGB_STEP_SL_GMRES = range(4)

@@ -13,3 +13,14 @@ void register_slgc() {
   REG_CL(2, 20);
 }
 }  // namespace mgb
+
+#ifdef MGB_CL_TRACE
+// trace builds only: fetch and clear the cluster-kernel phase timers
+extern "C" int mgb_trace_fetch(unsigned long long* out16) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, mgb::g_cl_trace, 16 * sizeof(unsigned long long));
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(mgb::g_cl_trace, z, sizeof(z));
+  return (int)cudaGetLastError();
+}
+#endif

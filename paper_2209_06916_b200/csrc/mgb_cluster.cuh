@@ -38,7 +38,7 @@ struct ClLayout {
   __host__ __device__ static int in_row(int) { return 0; }
   __host__ __device__ static int gm(int nc) { return nc; }
   __host__ __device__ static int wred(int nc) { return gm(nc) + nc + 2 * CL_H; }
-  __host__ __device__ static int cred(int nc) { return wred(nc) + CL_MAXW * N1; }
+  __host__ __device__ static int cred(int nc) { return wred(nc) + (N1 > CL_MAXW ? N1 : CL_MAXW) * N1; }
   __host__ __device__ static int tot(int nc) { return cred(nc) + 2 * CL_MAXC * N1; }
   __host__ __device__ static int hcol(int nc) { return tot(nc) + N1; }
   __host__ __device__ static int Rm(int nc) { return hcol(nc) + N1 + 1; }
@@ -49,7 +49,8 @@ struct ClLayout {
   __host__ __device__ static int bc(int nc) { return ybuf(nc) + N1; }
   __host__ __device__ static int mbar(int nc) { return bc(nc) + 8; }
   __host__ __device__ static int Z(int nc) { return mbar(nc) + 2; }
-  __host__ __device__ static int total(int nc) { return Z(nc) + N1 * nc; }
+  __host__ __device__ static int V(int nc) { return Z(nc) + N1 * nc; }
+  __host__ __device__ static int total(int nc) { return V(nc) + N1 * nc; }
 };
 
 struct ClCtx {
@@ -62,9 +63,6 @@ struct ClCtx {
   int t, T, nc, C, rank, base, lane, warp, nw, parity;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ uint32_t cl_map(uint32_t local, int rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
@@ -227,187 +225,246 @@ __device__ __forceinline__ void cl_publish(const ClCtx& c, const double (&w)[P])
   }
 }
 
+// CTA-partial dot products of the CTA slice `vec` with the basis rows Vs[i]
+// (i < nv) and, if `with_norm`, of vec with itself (value index nv).  One warp
+// per vector: coalesced lane-strided reads over the whole slice, one butterfly,
+// lane 0 stores the CTA partial -- no cross-warp stage.  Ends with a CTA barrier.
+__device__ __forceinline__ void cl_dots(ClCtx& c, const double* vec, const double* Vs, int nv,
+                                        bool with_norm, int wbeg = 0) {
+  const int cnt = nv + (with_norm ? 1 : 0);
+  for (int i = c.warp - wbeg; i < cnt && c.warp >= wbeg; i += c.nw - wbeg) {
+    const double* vi = i < nv ? Vs + (size_t)i * c.nc : vec;
+    double s0 = 0.0, s1 = 0.0;
+    int l = c.lane;
+    for (; l + 32 < c.nc; l += 64) {
+      s0 = fma(vec[l], vi[l], s0);
+      s1 = fma(vec[l + 32], vi[l + 32], s1);
+    }
+    if (l < c.nc) s0 = fma(vec[l], vi[l], s0);
+    double sv = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+    if (c.lane == 0) c.wred[i] = sv;
+  }
+  __syncthreads();
+}
+
+// Cluster exchange of the CTA partials c.wred[0..cnt): pushed into every CTA's
+// receive slots (double-buffered by parity), one cluster barrier, fixed
+// rank-order sums into c.tot[0..cnt) (identical in every CTA), CTA barrier.
+__device__ __forceinline__ void cl_exchange(ClCtx& c, int cnt, int N) {
+  const int p = c.parity;
+  double* cred = c.cred + p * (CL_MAXC * N);
+  if (c.t < cnt) {
+    const double s = c.wred[c.t];
+    const uint32_t src = smem_u32(cred) + 8u * (c.rank * N + c.t);
+    for (int r = 0; r < c.C; ++r) st_cluster_f64(cl_map(src, r), s);
+  }
+  cluster_barrier();  // peers' partials (and halo stores) visible
+  if (c.t < cnt) {  // pairwise tree over ranks (C is a power of two): depth log2(C)
+    double v[CL_MAXC];
+#pragma unroll
+    for (int r = 0; r < CL_MAXC; ++r) v[r] = r < c.C ? cred[r * N + c.t] : 0.0;
+#pragma unroll
+    for (int h = CL_MAXC / 2; h >= 1; h >>= 1)
+#pragma unroll
+      for (int r = 0; r < h; ++r) v[r] += v[r + h];
+    c.tot[c.t] = v[0];
+  }
+  __syncthreads();
+  c.parity ^= 1;
+}
+
 // Unrestarted GMRES(x0 = 0) on (I - phi D) for the cluster's distributed row
 // (semantics of circulant.py:262-332: stop when res <= tol or ||h|| <= 1e-14 beta,
 // Givens QR, back substitution, x = V y).  Arnoldi uses CGS2 with TWO cluster
 // reductions per step: pass 1 <w, V>, then pass 2 <w1, V> together with
 // ||w1||^2 (||w2||^2 = ||w1||^2 - ||h2||^2, explicit re-reduction if that
 // cancels) and w1's halo exchange; A v_{j+1} is updated linearly from A w1 and
-// Z = A V, so one stencil application per step.  The Givens update of column
-// j runs on thread 0 while the other warps start step j+1; its stop flag is
-// read after the next CTA barrier, before anything is sent.
+// Z = A V, so one stencil application per step.  V and Z live in shared memory
+// (each CTA its slice); all loops run to j, not to the cap.  Thread 0 keeps the
+// Hessenberg column and applies the Givens rotations; its stop flag is read
+// after the next CTA barrier.
 template <int P, int CAP>
 __device__ void cl_gmres(ClCtx& c, double* sm, const double (&b)[P],
                          double (&x)[P], int& depth_out, double& res_out) {
   const StepParams& sp = *c.sp;
   typedef ClLayout<CAP> LY;
   constexpr int N1 = CAP + 1;
-  const int cap = sp.cap;
+  const int cap = sp.cap, nc = c.nc;
   const int l0 = c.t * P;
-  double* hcol = sm + LY::hcol(c.nc);
-  double* Rm = sm + LY::Rm(c.nc);
-  double* cs = sm + LY::cs(c.nc);
-  double* sn = sm + LY::sn(c.nc);
-  double* gg = sm + LY::gg(c.nc);
-  double* ybuf = sm + LY::ybuf(c.nc);
-  double* bc = sm + LY::bc(c.nc);
-  double* Zs = sm + LY::Z(c.nc);  // Z_i = A v_i, own chunk per thread
+  double* hcol = sm + LY::hcol(nc);
+  double* Rm = sm + LY::Rm(nc);
+  double* cs = sm + LY::cs(nc);
+  double* sn = sm + LY::sn(nc);
+  double* gg = sm + LY::gg(nc);
+  double* ybuf = sm + LY::ybuf(nc);
+  double* bc = sm + LY::bc(nc);
+  double* Zs = sm + LY::Z(nc);   // Z_i = A v_i
+  double* Vs = sm + LY::V(nc);   // v_i
+  double* wv = c.gm + CL_H;      // the slice being orthogonalised (halo'd row)
+  CL_TR_INIT
 
   cl_publish<P>(c, b);
-  double nb[1] = {0.0};
-#pragma unroll
-  for (int q = 0; q < P; ++q) nb[0] = fma(b[q], b[q], nb[0]);
-  cl_sum<1>(c, nb, 1);  // its barrier also publishes b's halo values
-  const double beta = sqrt(nb[0]);
-#pragma unroll
-  for (int q = 0; q < P; ++q) x[q] = 0.0;
+  __syncthreads();
+  cl_dots(c, wv, Vs, 0, true);
+  cl_exchange(c, 1, N1);  // its barrier also publishes b's halos
+  const double beta = sqrt(c.tot[0]);
+  CL_TR(0)
   if (beta == 0.0) {  // zero right-hand side (circulant.py:274-278)
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] = 0.0;
     depth_out = 0;
     res_out = 0.0;
     return;
   }
   const double ib = 1.0 / beta;
-  double V[N1][P];
   {
     double z[P];
     cl_corr_apply<P>(c, z);
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      V[0][q] = b[q] * ib;
+      Vs[l0 + q] = b[q] * ib;
       Zs[l0 + q] = z[q] * ib;
     }
   }
-#pragma unroll
-  for (int i = 1; i < N1; ++i)
-#pragma unroll
-    for (int q = 0; q < P; ++q) V[i][q] = 0.0;
   if (c.t == 0) {
     gg[0] = beta;
     bc[0] = 1.0;
     bc[1] = 0.0;
   }
   int depth = 0;
-  for (int j = 0; j < cap; ++j) {
+  double hn_prev = 0.0;
+  bool happy_prev = false;
+  for (int j = 0;; ++j) {
     double w[P];
+    if (j < cap) {
 #pragma unroll
-    for (int q = 0; q < P; ++q) w[q] = Zs[j * c.nc + l0 + q];  // A v_j
-    double pd[N1];
-#pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      pd[i] = 0.0;
-      if (i <= j) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) pd[i] = fma(w[q], V[i][q], pd[i]);
+      for (int q = 0; q < P; ++q) {
+        w[q] = Zs[(size_t)j * nc + l0 + q];  // A v_j
+        wv[l0 + q] = w[q];
       }
     }
-    cl_sum_a<N1>(c, pd, j + 1);
-    if (bc[1] != 0.0) break;  // column j-1 converged or broke down (uniform)
-    cl_sum_b<N1>(c, pd, j + 1);
-#pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      if (i <= j) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(pd[i], V[i][q]));
-        if (c.t == 0) hcol[i] = pd[i];
+    __syncthreads();  // w, V_j, Z_j visible
+    if (c.warp == 0) {
+      if (c.t == 0 && j > 0) {  // Givens on column j-1 (h = h1 + h2), overlapped with the dots
+        const int jc = j - 1;
+        const double hn = hn_prev;
+        double hi = hcol[0] + c.tot[0];
+#pragma unroll 4
+        for (int i = 0; i < jc; ++i) {
+          const double ci = cs[i], si = sn[i], hi1 = hcol[i + 1] + c.tot[i + 1];
+          Rm[jc * CAP + i] = __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1));
+          hi = __dadd_rn(__dmul_rn(-si, hi), __dmul_rn(ci, hi1));
+        }
+        double den = hypot(hi, hn);
+        den = den > 0.0 ? den : 1.0;
+        const double rd = 1.0 / den;
+        const double cj = hi * rd, sj = hn * rd;
+        cs[jc] = cj;
+        sn[jc] = sj;
+        Rm[jc * CAP + jc] = __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn));
+        const double gj = gg[jc];
+        gg[jc + 1] = __dmul_rn(-sj, gj);
+        gg[jc] = __dmul_rn(cj, gj);
+        const double r = fabs(gg[jc + 1]) / beta;
+        bc[0] = r;
+        bc[1] = (!(r > sp.tol) || happy_prev) ? 1.0 : 0.0;
+      }
+      if (c.nw == 1 && j < cap) {
+        cl_dots(c, wv, Vs, j + 1, false, 0);  // single warp: no spare warps to overlap with
+      } else {
+        __syncthreads();  // the dot warps' barrier (cl_dots ends with one)
+      }
+    } else {
+      if (j < cap) {
+        cl_dots(c, wv, Vs, j + 1, false, 1);
+      } else {
+        __syncthreads();
       }
     }
-    cl_publish<P>(c, w);  // w1 halos complete on the pass-2 barrier
+    CL_TR(1)
+    depth = j;
+    if (j == cap || bc[1] != 0.0) break;  // uniform
+    cl_exchange(c, j + 1, N1);
+    CL_TR(2)
+    if (c.t <= j) hcol[c.t] = c.tot[c.t];  // h1 (thread i owns entry i)
+    for (int i = 0; i <= j; ++i) {
+      const double h = c.tot[i];
 #pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      double d = 0.0;
-      if (i <= j) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) d = fma(w[q], V[i][q], d);
-      } else if (i == j + 1) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) d = fma(w[q], w[q], d);
-      }
-      pd[i] = d;
+      for (int q = 0; q < P; ++q) w[q] = fma(-h, Vs[(size_t)i * nc + l0 + q], w[q]);
     }
-    cl_sum<N1>(c, pd, j + 2);  // barrier also publishes w1's halos
+    cl_publish<P>(c, w);  // w1 into the halo'd row + neighbours' halos
+    __syncthreads();
+    CL_TR(3)
+    cl_dots(c, wv, Vs, j + 1, true);
+    cl_exchange(c, j + 2, N1);  // barrier also publishes w1's halos
+    CL_TR(4)
     double aw[P];
     cl_corr_apply<P>(c, aw);  // A w1
-    double s1 = 0.0, hh = 0.0;
+    double hh0 = 0.0, hh1 = 0.0;
+    for (int i = 0; i <= j; ++i) {
+      const double h = c.tot[i];
+      if (i & 1) hh1 = fma(h, h, hh1); else hh0 = fma(h, h, hh0);
 #pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      if (i <= j) {
-        hh = fma(pd[i], pd[i], hh);
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-          w[q] = __dsub_rn(w[q], __dmul_rn(pd[i], V[i][q]));
-          aw[q] = __dsub_rn(aw[q], __dmul_rn(pd[i], Zs[i * c.nc + l0 + q]));
-        }
-        if (c.t == 0) hcol[i] += pd[i];
-      } else if (i == j + 1) {
-        s1 = pd[i];
+      for (int q = 0; q < P; ++q) {
+        w[q] = fma(-h, Vs[(size_t)i * nc + l0 + q], w[q]);
+        aw[q] = fma(-h, Zs[(size_t)i * nc + l0 + q], aw[q]);
       }
     }
-    double hn2 = s1 - hh;
+    const double s1 = c.tot[j + 1];
+    double hn2 = s1 - (hh0 + hh1);
     if (!(hn2 >= 1e-6 * s1)) {  // cancellation: explicit ||w2||^2 (uniform branch)
-      double e[1] = {0.0};
+      __syncthreads();
 #pragma unroll
-      for (int q = 0; q < P; ++q) e[0] = fma(w[q], w[q], e[0]);
-      cl_sum<1>(c, e, 1);
-      hn2 = e[0];
+      for (int q = 0; q < P; ++q) wv[l0 + q] = w[q];
+      __syncthreads();
+      double hsave = c.t <= j ? c.tot[c.t] : 0.0;  // keep h2 for the Givens
+      cl_dots(c, wv, Vs, 0, true);
+      cl_exchange(c, 1, N1);
+      hn2 = c.tot[0];
+      __syncthreads();
+      if (c.t <= j) c.tot[c.t] = hsave;
+      __syncthreads();
     }
     const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
-    const bool happy = hn <= 1e-14 * beta;
+    CL_TR(5)
+    happy_prev = hn <= 1e-14 * beta;
+    hn_prev = hn;
     const double inv = 1.0 / (hn > 0.0 ? hn : 1.0);
-#pragma unroll
-    for (int i = 1; i < N1; ++i) {  // select form keeps V in registers
-#pragma unroll
-      for (int q = 0; q < P; ++q) V[i][q] = (i == j + 1) ? w[q] * inv : V[i][q];
-    }
     if (j + 1 < N1) {
 #pragma unroll
-      for (int q = 0; q < P; ++q) Zs[(j + 1) * c.nc + l0 + q] = aw[q] * inv;
-    }
-    if (c.t == 0) {  // Givens on column j (identical in every CTA)
-      // the rotated entry is carried in a register; cs/sn/h loads are off the chain
-      double hi = hcol[0];
-#pragma unroll 4
-      for (int i = 0; i < j; ++i) {
-        const double ci = cs[i], si = sn[i], hi1 = hcol[i + 1];
-        hcol[i] = __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1));
-        hi = __dadd_rn(__dmul_rn(-si, hi), __dmul_rn(ci, hi1));
+      for (int q = 0; q < P; ++q) {
+        Vs[(size_t)(j + 1) * nc + l0 + q] = w[q] * inv;
+        Zs[(size_t)(j + 1) * nc + l0 + q] = aw[q] * inv;
       }
-      double den = hypot(hi, hn);
-      den = den > 0.0 ? den : 1.0;
-      const double cj = hi / den, sj = hn / den;
-      cs[j] = cj;
-      sn[j] = sj;
-      hcol[j] = __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn));
-      const double gj = gg[j];
-      gg[j + 1] = __dmul_rn(-sj, gj);
-      gg[j] = __dmul_rn(cj, gj);
-      const double r = fabs(gg[j + 1]) / beta;
-      for (int i = 0; i <= j; ++i) Rm[j * CAP + i] = hcol[i];
-      bc[0] = r;
-      bc[1] = (!(r > sp.tol) || happy) ? 1.0 : 0.0;
     }
-    depth = j + 1;
+    CL_TR(6)
+#ifdef MGB_CL_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_cl_trace[15], 1ull);
+#endif
   }
   __syncthreads();
-  const double res = bc[0];
-  if (c.t == 0) {
-    for (int i = 0; i < depth; ++i) ybuf[i] = gg[i];
+  const double res = depth > 0 ? bc[0] : 1.0;
+  if (c.warp == 0) {  // back substitution R y = g, column oriented, lanes own rows
+    double y = c.lane < depth ? gg[c.lane] : 0.0;
     for (int jj = depth - 1; jj >= 0; --jj) {
-      if (ybuf[jj] != 0.0) {
-        ybuf[jj] /= Rm[jj * CAP + jj];
-        const double yj = ybuf[jj];
-        for (int i = 0; i < jj; ++i) ybuf[i] = __dsub_rn(ybuf[i], __dmul_rn(yj, Rm[jj * CAP + i]));
-      }
+      double yj = __shfl_sync(0xffffffffu, y, jj);
+      if (yj != 0.0) yj /= Rm[jj * CAP + jj];
+      if (c.lane == jj) y = yj;
+      if (c.lane < jj) y = fma(-yj, Rm[jj * CAP + c.lane], y);
     }
+    if (c.lane < depth) ybuf[c.lane] = y;
   }
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < N1; ++i) {
-    if (i < depth) {
-      const double yi = ybuf[i];
+  for (int q = 0; q < P; ++q) x[q] = 0.0;
+  for (int i = 0; i < depth; ++i) {
+    const double yi = ybuf[i];
 #pragma unroll
-      for (int q = 0; q < P; ++q) x[q] = __dadd_rn(x[q], __dmul_rn(yi, V[i][q]));
-    }
+    for (int q = 0; q < P; ++q) x[q] = fma(yi, Vs[(size_t)i * nc + l0 + q], x[q]);
   }
+  CL_TR(7)
   depth_out = depth;
   res_out = res;
 }
@@ -488,8 +545,11 @@ __global__ void __launch_bounds__(256) relax_cluster_kernel(const StepParams* __
     for (int j = 1; j <= nsteps; ++j) {
       const bool is_tail = j > a.n_fsteps;
       double b[P];
+      CL_TR_INIT
       cl_sl_apply<P>(c, cl, b);
+      CL_TR(8)
       cl_gmres<P, CAP>(c, sm, b, y, depth, gres);
+      CL_TR(14)
       const long long grow = is_tail ? rowbase + a.m : rowbase + j;
       if (!is_tail) {
         if (a.g) {
@@ -503,6 +563,7 @@ __global__ void __launch_bounds__(256) relax_cluster_kernel(const StepParams* __
         for (int q = 0; q < P; ++q) c.in_row[t * P + q] = y[q];
         if (a.write_f == 2 || (a.write_f == 1 && j == a.n_fsteps)) cl_store<P>(a.u + grow * n, c, y);
         cluster_barrier();  // the next SL step reads peers' rows
+        CL_TR(9)
       } else if (a.tail == 1) {
         if (a.g) {
           double gv[P];

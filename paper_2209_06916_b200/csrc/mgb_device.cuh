@@ -19,6 +19,25 @@
 
 namespace mgb {
 
+// Optional phase timers (trace builds only: -DMGB_CL_TRACE): clock64 deltas of
+// thread 0 of block 0, accumulated per phase (one buffer per translation unit).
+#ifdef MGB_CL_TRACE
+__device__ unsigned long long g_cl_trace[16];
+#define CL_TR_INIT long long cl_t0_ = clock64();
+#define CL_TR(k)                                                                      \
+  if (threadIdx.x == 0 && blockIdx.x == 0) {                                          \
+    const long long t_ = clock64();                                                   \
+    atomicAdd(&g_cl_trace[k], (unsigned long long)(t_ - cl_t0_));                    \
+    cl_t0_ = t_;                                                                      \
+  }
+#define CL_TR_STEP \
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_cl_trace[15], 1ull);
+#else
+#define CL_TR_INIT
+#define CL_TR(k)
+#define CL_TR_STEP
+#endif
+
 constexpr int MAXP = 16;
 constexpr int MAX_TAPS = 256;
 constexpr int MAX_TAPS2 = 32;
@@ -68,6 +87,30 @@ struct RelaxLaunch {
 };
 
 // ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  }
+}
+// TMA bulk copy global -> shared (one instruction, completes tx bytes on `bar`)
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 
 template <bool EXACT>
 __device__ __forceinline__ double madd(double acc, double w, double v) {
@@ -135,6 +178,7 @@ struct Ctx {
   int t, T, S, n;
   bool own;
   int parity;
+  unsigned phase;  // GMRES stage mbarrier phases
 };
 
 // Deterministic block reduction: warp butterfly, one CTA barrier, then every
@@ -365,7 +409,7 @@ template <int P>
 __device__ __forceinline__ void apply_op2(const Ctx& c, double (&y)[P]) {
   const StepParams& sp = *c.sp;
   if (!sp.win2_ok) {
-    stencil_gen<P, true>(c, sp.ntap2, sp.tap2_off, sp.tap2_w, y);
+    stencil_gen<P, false>(c, sp.ntap2, sp.tap2_off, sp.tap2_w, y);
     return;
   }
 #pragma unroll
@@ -390,17 +434,34 @@ __device__ __forceinline__ void apply_op2(const Ctx& c, double (&y)[P]) {
     if (k <= span) {
       const double wk = sp.win2_w[k];
 #pragma unroll
-      for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], __dmul_rn(wk, win[q + k]));
+      for (int q = 0; q < P; ++q) y[q] = fma(wk, win[q + k], y[q]);  // inside GMRES: DFMA
     }
   }
 }
 
+constexpr int RS_CAP = 24;  // Hessenberg R kept in shared memory for cap <= RS_CAP
+
+// Shared-memory carve-up of the single-CTA GMRES (after the scan area), doubles
+struct GmLayout {
+  __host__ __device__ static int hcol() { return 0; }
+  __host__ __device__ static int ybuf() { return MAX_CAP + 2; }
+  __host__ __device__ static int cs() { return ybuf() + MAX_CAP; }
+  __host__ __device__ static int sn() { return cs() + MAX_CAP; }
+  __host__ __device__ static int gg() { return sn() + MAX_CAP; }
+  __host__ __device__ static int Rs() { return gg() + MAX_CAP + 2; }
+  __host__ __device__ static int mbar() { return Rs() + RS_CAP * RS_CAP; }
+  __host__ __device__ static int stage() { return mbar() + 4; }  // + 16-byte alignment pad
+  __host__ __device__ static int total(int n) { return stage() + 2 + 2 * n; }
+};
+
 // Unrestarted GMRES(x0 = 0) on the circulant (taps2) for the CTA's row,
 // following circulant.py:262-332: MGS Arnoldi, Givens QR, stop when
 // res <= tol or ||h|| <= 1e-14 beta, back substitution, x = V y.
-// V lives in this CTA's HBM/L2 workspace slot (coalesced 16-byte layout, next
-// vector prefetched); Givens/g/cs/sn on thread 0 with the rotated entry in a
-// register; normalisations multiply by the reciprocal.
+// The basis V lives in this CTA's L2/HBM workspace slot (16-byte coalesced
+// layout); the vectors an Arnoldi step needs are streamed into two shared
+// memory stages with TMA bulk copies (cp.async.bulk + mbarrier) two ahead of
+// use, so MGS reads them at shared-memory latency.  R and the Givens state
+// stay in shared memory; the back substitution runs on one warp.
 template <int P>
 __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& depth_out,
                             double& res_out) {
@@ -408,19 +469,37 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   const int n = c.n, T = c.T, t = c.t;
   const int cap = sp.cap;
   double* V = c.ws;
-  double* R = V + (size_t)(cap + 1) * n;
-  double* hcol = c.gm;
-  double* ybuf = hcol + MAX_CAP + 2;
-  double* cs = ybuf + MAX_CAP;
-  double* sn = cs + MAX_CAP;
-  double* gg = sn + MAX_CAP;
-
+  double* Rg = V + (size_t)(cap + 1) * n;  // global R (cap > RS_CAP only)
+  double* hcol = c.gm + GmLayout::hcol();
+  double* ybuf = c.gm + GmLayout::ybuf();
+  double* cs = c.gm + GmLayout::cs();
+  double* sn = c.gm + GmLayout::sn();
+  double* gg = c.gm + GmLayout::gg();
+  double* R = cap <= RS_CAP ? c.gm + GmLayout::Rs() : Rg;
+  const int ldr = cap <= RS_CAP ? RS_CAP : cap;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(c.gm + GmLayout::mbar());
+  double* stage0 = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(c.gm + GmLayout::stage()) + 15) & ~uintptr_t(15));
+  const uint32_t vbytes = (uint32_t)n * 8u;
+#define MGB_ISSUE(i, st)                                                      \
+  do {                                                                        \
+    mbar_arm(bar + (st), vbytes);                                             \
+    bulk_g2s(stage0 + (size_t)(st) * n, V + (size_t)(i) * n, vbytes, bar + (st)); \
+  } while (0)
+#define MGB_CONSUME(st, vi)                                                   \
+  do {                                                                        \
+    mbar_wait(bar + (st), (c.phase >> (st)) & 1u);                            \
+    c.phase ^= 1u << (st);                                                    \
+    if (c.own) vec_load<P>(stage0 + (size_t)(st) * n, t, T, vi);              \
+  } while (0)
+  CL_TR_INIT
   double part = 0.0;
   if (c.own) {
 #pragma unroll
     for (int q = 0; q < P; ++q) part = fma(b[q], b[q], part);
   }
   const double beta = sqrt(block_sum(c, part));
+  CL_TR(0)
   if (beta == 0.0) {  // zero right-hand side: x = 0, converged (circulant.py:274-278)
 #pragma unroll
     for (int q = 0; q < P; ++q) x[q] = 0.0;
@@ -433,6 +512,7 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
 #pragma unroll
   for (int q = 0; q < P; ++q) v[q] = b[q] * ib;
   if (c.own) vec_store<P>(V, t, T, v);
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> TMA reads
   if (t == 0) gg[0] = beta;
   double res = 1.0;
   int depth = 0;
@@ -440,18 +520,22 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
     __syncthreads();
     if (c.own) chunk_to_row<P>(c.row, t, c.S, v);
     __syncthreads();
+    if (t == 0) {  // stream V_0, V_1 while the stencil runs (V_j itself is the row)
+      if (j >= 1) MGB_ISSUE(0, 0);
+      if (j >= 2) MGB_ISSUE(1, 1);
+    }
+    CL_TR(9)
     double w[P];
     apply_op2<P>(c, w);
-    // modified Gram-Schmidt (next basis vector prefetched from L2)
-    double vn[P];
+    CL_TR(1)
+    for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+      double vi[P];
+      if (i < j) {
+        MGB_CONSUME(i & 1, vi);
+      } else {
 #pragma unroll
-    for (int q = 0; q < P; ++q) vn[q] = 0.0;
-    if (c.own && j > 0) vec_load<P>(V, t, T, vn);
-    for (int i = 0; i <= j; ++i) {
-      double vi[P];  // v_j itself is re-read from the resident row (keeps v dead here)
-#pragma unroll
-      for (int q = 0; q < P; ++q) vi[q] = (i == j) ? (c.own ? c.row[q * c.S + t] : 0.0) : vn[q];
-      if (c.own && i + 1 < j) vec_load<P>(V + (size_t)(i + 1) * n, t, T, vn);
+        for (int q = 0; q < P; ++q) vi[q] = c.own ? c.row[q * c.S + t] : 0.0;
+      }
       double p0 = 0.0, p1 = 0.0;
       if (c.own) {
 #pragma unroll
@@ -460,10 +544,15 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
           if (q + 1 < P) p1 = fma(w[q + 1], vi[q + 1], p1);
         }
       }
-      const double h = block_sum(c, p0 + p1);
-      if (t == 0) hcol[i] = h;
+      CL_TR(2)
+      const double h = block_sum(c, p0 + p1);  // every thread has consumed stage i&1
+      CL_TR(3)
+      if (t == 0) {
+        hcol[i] = h;
+        if (i + 2 < j) MGB_ISSUE(i + 2, i & 1);
+      }
 #pragma unroll
-      for (int q = 0; q < P; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(h, vi[q]));
+      for (int q = 0; q < P; ++q) w[q] = fma(-h, vi[q], w[q]);
     }
     double n0 = 0.0, n1 = 0.0;
     if (c.own) {
@@ -473,61 +562,87 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
         if (q + 1 < P) n1 = fma(w[q + 1], w[q + 1], n1);
       }
     }
+    CL_TR(4)
     const double hn = sqrt(block_sum(c, n0 + n1));
+    CL_TR(5)
     const bool happy = hn <= 1e-14 * beta;
     const double inv = 1.0 / (hn > 0.0 ? hn : 1.0);
 #pragma unroll
     for (int q = 0; q < P; ++q) v[q] = w[q] * inv;
     if (c.own) vec_store<P>(V + (size_t)(j + 1) * n, t, T, v);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     if (t == 0) {  // Givens (circulant.py:308-319), rotated entry carried in a register
       double hi = hcol[0];
 #pragma unroll 4
       for (int i = 0; i < j; ++i) {
         const double ci = cs[i], si = sn[i], hi1 = hcol[i + 1];
-        hcol[i] = __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1));
+        R[(size_t)j * ldr + i] = __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1));
         hi = __dadd_rn(__dmul_rn(-si, hi), __dmul_rn(ci, hi1));
       }
       double den = hypot(hi, hn);
       den = den > 0.0 ? den : 1.0;
-      const double cj = hi / den, sj = hn / den;
+      const double rd = 1.0 / den;
+      const double cj = hi * rd, sj = hn * rd;
       cs[j] = cj;
       sn[j] = sj;
-      hcol[j] = __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn));
+      R[(size_t)j * ldr + j] = __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn));
       const double gj = gg[j];
       gg[j + 1] = __dmul_rn(-sj, gj);
       gg[j] = __dmul_rn(cj, gj);
       const double r = fabs(gg[j + 1]) / beta;
-      for (int i = 0; i <= j; ++i) R[(size_t)j * cap + i] = hcol[i];
       c.bc[0] = r;
       c.bc[1] = (!(r > sp.tol) || happy) ? 1.0 : 0.0;
     }
+    CL_TR(6)
     __syncthreads();
+    CL_TR(7)
+    CL_TR_STEP
     res = c.bc[0];
     depth = j + 1;
     if (c.bc[1] != 0.0) break;
   }
-  if (t == 0) {  // back substitution on the rotated (upper triangular) H
-    for (int i = 0; i < depth; ++i) ybuf[i] = gg[i];
-    for (int jj = depth - 1; jj >= 0; --jj) {
-      if (ybuf[jj] != 0.0) {
-        ybuf[jj] /= R[(size_t)jj * cap + jj];
-        const double yj = ybuf[jj];
-        for (int i = 0; i < jj; ++i) ybuf[i] = __dsub_rn(ybuf[i], __dmul_rn(yj, R[(size_t)jj * cap + i]));
+  const int lane = t & 31;
+  if ((t >> 5) == 0) {  // back substitution R y = g, column oriented, lanes own rows
+    if (depth <= 32) {
+      double y = lane < depth ? gg[lane] : 0.0;
+      for (int jj = depth - 1; jj >= 0; --jj) {
+        double yj = __shfl_sync(0xffffffffu, y, jj);
+        if (yj != 0.0) yj /= R[(size_t)jj * ldr + jj];
+        if (lane == jj) y = yj;
+        if (lane < jj) y = __dsub_rn(y, __dmul_rn(yj, R[(size_t)jj * ldr + lane]));
+      }
+      if (lane < depth) ybuf[lane] = y;
+    } else if (lane == 0) {
+      for (int i = 0; i < depth; ++i) ybuf[i] = gg[i];
+      for (int jj = depth - 1; jj >= 0; --jj) {
+        if (ybuf[jj] != 0.0) {
+          ybuf[jj] /= R[(size_t)jj * ldr + jj];
+          const double yj = ybuf[jj];
+          for (int i = 0; i < jj; ++i) ybuf[i] = __dsub_rn(ybuf[i], __dmul_rn(yj, R[(size_t)jj * ldr + i]));
+        }
       }
     }
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < P; ++q) x[q] = 0.0;
-  if (c.own) {
-    double vi[P];
+  if (c.own) {  // x = V y: basis streamed from L2 with a two-deep register prefetch
+    double va[P], vb[P];
+    vec_load<P>(V, t, T, va);
+    if (depth > 1) vec_load<P>(V + n, t, T, vb);
     for (int i = 0; i < depth; ++i) {
       const double yi = ybuf[i];
-      vec_load<P>(V + (size_t)i * n, t, T, vi);
 #pragma unroll
-      for (int q = 0; q < P; ++q) x[q] = __dadd_rn(x[q], __dmul_rn(yi, vi[q]));
+      for (int q = 0; q < P; ++q) {
+        x[q] = fma(yi, va[q], x[q]);
+        va[q] = vb[q];
+      }
+      if (i + 2 < depth) vec_load<P>(V + (size_t)(i + 2) * n, t, T, vb);
     }
   }
+#undef MGB_ISSUE
+#undef MGB_CONSUME
+  CL_TR(8)
   depth_out = depth;
   res_out = res;
 }
@@ -593,8 +708,9 @@ __device__ __forceinline__ void step_once(Ctx& c, const double (&wd)[SPAN + 1], 
 
 __host__ __device__ constexpr int sp_bytes() { return (int)sizeof(StepParams); }
 
-template <int P, int KIND, int SPAN, int NST, bool EXACT>
-__global__ void __launch_bounds__(512) relax_kernel(const StepParams* __restrict__ gp, const RelaxLaunch L) {
+// MAXT: launch bound (512, or 256 for register-heavy GMRES variants, T <= 256)
+template <int P, int KIND, int SPAN, int NST, bool EXACT, int MAXT = 512>
+__global__ void __launch_bounds__(MAXT) relax_kernel(const StepParams* __restrict__ gp, const RelaxLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   {
     const int4* src = reinterpret_cast<const int4*>(gp);
@@ -618,6 +734,16 @@ __global__ void __launch_bounds__(512) relax_kernel(const StepParams* __restrict
   c.gm = c.scan + ((KIND == K_SLD || KIND == K_RK) ? 4 * c.T : 0);
   c.ws = L.ws ? L.ws + (size_t)blockIdx.x * L.ws_slot : nullptr;
   c.parity = 0;
+  c.phase = 0;
+  if constexpr (KIND == K_SLG) {
+    if (threadIdx.x == 0) {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(c.gm + GmLayout::mbar());
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   const int n = c.n, t = c.t;
 
   double wd[SPAN + 1];

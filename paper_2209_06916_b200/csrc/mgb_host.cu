@@ -334,7 +334,7 @@ void prepare_clusters(mgb_step* st) {
     if (n % C) continue;
     const int nc = n / C;
     int P = 0;
-    for (int p : {2, 1})
+    for (int p : {1, 2})  // most warps (up to 8) for the warp-per-vector dot products
       if (nc % p == 0 && nc / p <= 256 && nc / p >= 32 && (nc / p) % 32 == 0) {
         P = p;
         break;
@@ -499,11 +499,14 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->threads = ((T + 31) / 32) * 32;
   size_t dbl = (size_t)P * S + 64 + 8;
   if (dk == mgb::K_RK || dk == mgb::K_SLD) dbl += 4 * (size_t)T;
-  if (dk == mgb::K_SLG) dbl += 5 * mgb::MAX_CAP + 4;  // hcol, y, cs, sn, g
+  if (dk == mgb::K_SLG) dbl += mgb::GmLayout::total(n);  // Hessenberg state, R, 2 TMA stages
   st->smem = (int)(sizeof(StepParams) + 8 * dbl);
   {
     std::lock_guard<std::mutex> lk(reg_mutex());
-    auto it = registry().find(std::make_tuple(dk, P, span, st->nst, st->exact));
+    auto it = registry().end();
+    if (dk == mgb::K_SLG && T <= 256)  // register-rich variant (launch bound 256)
+      it = registry().find(std::make_tuple(dk, P, span, 2, st->exact));
+    if (it == registry().end()) it = registry().find(std::make_tuple(dk, P, span, st->nst, st->exact));
     if (it == registry().end()) { delete st; return fail(MGB_ERR_UNSUPPORTED, "no kernel instantiation for this layout"); }
     st->fn = it->second;
   }
@@ -569,8 +572,10 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   long long grid = std::min<long long>(a->n_intervals, st->max_grid);
   static const bool no_cluster = std::getenv("MGB_NO_CLUSTER") != nullptr;
   if (st->dkind == mgb::K_SLG && !no_cluster) {
-    for (const ClusterVariant& v : st->clusters) {  // largest cluster size that runs in one wave
-      if (a->n_intervals > (long long)v.max_clusters) continue;
+    static const long long max_waves = std::getenv("MGB_CLUSTER_WAVES")
+                                           ? std::atoll(std::getenv("MGB_CLUSTER_WAVES")) : 2;
+    for (const ClusterVariant& v : st->clusters) {  // largest cluster size within max_waves
+      if (a->n_intervals > max_waves * (long long)v.max_clusters) continue;
       const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(ncl * v.C));
