@@ -119,6 +119,27 @@ def algorithmic_work(cf, solver, name):
     return "latency", None
 
 
+def fp64_peak_gflops() -> float:
+    """Measured FP64 DFMA throughput of this GPU (GFLOP/s), CUDA events."""
+    import ctypes
+    import torch
+    from paper_2209_06916_b200 import _native
+    lib = _native.load()
+    fl = ctypes.c_double()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    lib.mgb_fp64_peak(1000, ctypes.byref(fl), stream)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        lib.mgb_fp64_peak(20000, ctypes.byref(fl), stream)
+        e.record()
+        torch.cuda.synchronize()
+        best = max(best, fl.value / (s.elapsed_time(e) / 1e3) / 1e9)
+    return best
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -204,10 +225,32 @@ def run_gpu(args):
         bound, work = algorithmic_work(cf, solver, "L0.CF")
         per_launch_s = fine_cf[1] / fine_cf[0] / 1e3
         ach = work / per_launch_s / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tr = json.load(f).get("L0.CF")
+            if tr:
+                traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+        except Exception:
+            pass
         roof = {"bound": "hbm", "kernel": "relax_kernel L0.CF (correct + F-relax + residual)",
                 "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(ach / hbm_peak, 4), "peak_source": peak_kind,
-                "traffic": None, "share_of_step": round(fine_cf[1] / total_ms, 4)}
+                "algorithmic_bytes": work, "traffic": traffic,
+                "traffic_source": "profiles/traffic.json (ncu --set full, one launch)",
+                "share_of_step": round(fine_cf[1] / total_ms, 4)}
+    roof_fp64 = None
+    fine_fc = passes.get("L0.FC")
+    if fine_fc:
+        fp64_peak = fp64_peak_gflops()
+        _, flops = algorithmic_work(cf, solver, "L0.FC")
+        ach = flops / (fine_fc[1] / fine_fc[0] / 1e3) / 1e9
+        roof_fp64 = {"bound": "fp64", "kernel": "relax_kernel L0.FC (F-relax + C-relax, exact mode)",
+                     "achieved": round(ach, 1), "peak": round(fp64_peak, 1), "unit": "GFLOP/s",
+                     "frac": round(ach / fp64_peak, 4),
+                     "peak_source": "measured live: DFMA probe (mgb_fp64_peak), 2 flop/DFMA",
+                     "note": "exact mode issues DMUL+DADD per tap (2 flop in 2 issue slots): "
+                             "the pipe-time bound is half the DFMA peak"}
     breakdown = {k: {"launches": c, "ms": round(ms, 4), "share": round(ms / total_ms, 4)}
                  for k, (c, ms) in sorted(passes.items(), key=lambda kv: -kv[1][1])}
 
@@ -230,6 +273,7 @@ def run_gpu(args):
                 "seconds": e2e_s},
         "gpu_launches": launches,
         "roofline": roof,
+        "roofline_fp64": roof_fp64,
         "dominant_pass": {"name": dom[0], "share": round(dom[1][1] / total_ms, 4)},
         "passes": breakdown,
         "clocks": clk.summary(),

@@ -126,6 +126,10 @@ int mgb_relax(mgb_step* step, const mgb_relax_args* args, void* stream);
  * Backs np.linalg.norm in cpoint_residual_norm (mgrit.py:164-166). */
 int mgb_sum(const double* partials, int64_t n, double* out, void* stream);
 
+/* Diagnostics: launch the FP64 (DFMA) throughput probe used as the FP64
+ * roofline denominator by bench.py; *flops_per_launch receives its flop count. */
+int mgb_fp64_peak(int64_t iters, double* flops_per_launch, void* stream);
+
 /* Library identification and error text. */
 int mgb_version(void);
 const char* mgb_last_error(void);

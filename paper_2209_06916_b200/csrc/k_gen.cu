@@ -31,3 +31,31 @@ extern "C" int mgb_trace_fetch_gen(unsigned long long* out16) {
   return (int)cudaGetLastError();
 }
 #endif
+
+// FP64 pipe peak probe: 8 independent DFMA chains per thread, every SM busy.
+namespace mgb {
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, long long iters) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  const double b = 0.999999999, c = 1e-12;
+  for (long long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the work alive
+}
+}  // namespace mgb
+
+extern "C" int mgb_fp64_peak(int64_t iters, double* flops_per_launch, void* stream) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 8, threads = 256;
+  mgb::fp64_peak_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(nullptr, (long long)iters);
+  if (flops_per_launch) *flops_per_launch = 2.0 * 8.0 * (double)iters * blocks * threads;
+  return (int)cudaGetLastError();
+}

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "mgrit_b200.h")).read()
-    return sorted(set(re.findall(r"\b(mgb_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(mgb_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_exported_list():
