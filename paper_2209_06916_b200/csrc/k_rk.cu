@@ -17,3 +17,13 @@ void register_rk() {
   RK_P(16)
 }
 }  // namespace mgb
+
+#ifdef MGB_CL_TRACE
+extern "C" int mgb_trace_fetch_rk(unsigned long long* out16) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, mgb::g_cl_trace, 16 * sizeof(unsigned long long));
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(mgb::g_cl_trace, z, sizeof(z));
+  return (int)cudaGetLastError();
+}
+#endif

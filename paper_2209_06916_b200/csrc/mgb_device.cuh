@@ -55,7 +55,7 @@ enum { K_WIN = 0, K_GEN = 1, K_RK = 2, K_SLD = 3, K_SLG = 4, K_SLGC = 5 };
 // Tables are precomputed in long double for the launch geometry (T, P).
 struct Factor {
   double a1, a2;
-  int dir, pad_;
+  int dir, win;  // win > 0: carries by windowed look-back over win chunks
   double h1[MAXP], h2[MAXP];  // first row of A^(q+1): response to the carry-in state
   double M[4];                // A^P: chunk transition
   double Mpow[LOGT][4];       // M^(2^k)
@@ -67,7 +67,7 @@ struct StepParams {
   int kind, n, P, T, S, exact, repeat, stages;
   int implicit, nfac, shift, cap;
   int ntap, ntap2, win_lo, win_span;
-  int win2_lo, win2_span, win2_ok, pad2_;  // contiguous implicit stencil (GMRES operator)
+  int win2_lo, win2_span, win2_ok, win1_ok;  // contiguous stencils: GMRES operator / RK -cL
   double gain_inv, tol;
   double A[MAX_ST * MAX_ST], b[MAX_ST];
   int tap_off[MAX_TAPS];
@@ -258,18 +258,26 @@ __device__ __forceinline__ void mv2(const double* M, double& x1, double& x2) {
   x2 = n2;
 }
 
+// Carry-state storage for the factor scans: component-split arrays, chunk tl
+// at (tl % R) * 33 + tl / R (R = chunks per lane of warp 0): conflict-free for
+// warp 0's lane-strided scan, at most 2-way for the chunk-owner writes.
+__host__ __device__ __forceinline__ int scan_R(int T) { return T <= 32 ? 1 : (T + 31) >> 5; }
+__device__ __forceinline__ int scan_addr(int tl, int R) { return (tl % R) * 33 + tl / R; }
+__host__ __device__ __forceinline__ int scan_stride(int T) { return 33 * scan_R(T) + 33; }
+
 // warp 0: carry-in states of all logical chunks for one factor.
 __device__ __forceinline__ void lane_scan(const Factor& F, const double* st, double* cin, double* sb,
                                           int T, int lane) {
   const int R = (T + 31) >> 5;
+  const int SS = scan_stride(T);
   const int base = lane * R;
   double X1 = 0.0, X2 = 0.0;
   for (int i = 0; i < R; ++i) {
     const int tl = base + i;
     double b1 = 0.0, b2 = 0.0;
     if (tl < T) {
-      b1 = st[2 * tl];
-      b2 = st[2 * tl + 1];
+      b1 = st[scan_addr(tl, R)];
+      b2 = st[SS + scan_addr(tl, R)];
     }
     mv2(F.M, X1, X2);
     X1 += b1;
@@ -293,11 +301,11 @@ __device__ __forceinline__ void lane_scan(const Factor& F, const double* st, dou
   for (int i = 0; i < R; ++i) {
     const int tl = base + i;
     if (tl < T) {
-      cin[2 * tl] = s1;
-      cin[2 * tl + 1] = s2;
+      cin[scan_addr(tl, R)] = s1;
+      cin[SS + scan_addr(tl, R)] = s2;
       mv2(F.M, s1, s2);
-      s1 += st[2 * tl];
-      s2 += st[2 * tl + 1];
+      s1 += st[scan_addr(tl, R)];
+      s2 += st[SS + scan_addr(tl, R)];
       if (tl == T - 1) {  // zero-start end state -> periodic closure
         double w1 = s1, w2 = s2;
         mv2(F.Winv, w1, w2);
@@ -308,13 +316,85 @@ __device__ __forceinline__ void lane_scan(const Factor& F, const double* st, dou
   }
 }
 
+struct M2r {
+  double a, b, c, d;
+};
+__device__ __forceinline__ M2r ld_m2(const double* M) { return {M[0], M[1], M[2], M[3]}; }
+__device__ __forceinline__ void mv2r(const M2r& M, double& x1, double& x2) {
+  const double n1 = fma(M.a, x1, M.b * x2);
+  const double n2 = fma(M.c, x1, M.d * x2);
+  x1 = n1;
+  x2 = n2;
+}
+
+// warp 0: TRUE carry-in states (periodic closure included) of all logical
+// chunks for one factor; requires T % 32 == 0 or T <= 32 (exact R chunks/lane).
+// Transition matrices live in registers for the whole scan.
+__device__ __forceinline__ void lane_scan_true(const Factor& F, const double* st, double* cin,
+                                               int T, int lane) {
+  const int R = T <= 32 ? 1 : (T >> 5);
+  const int SS = scan_stride(T);
+  const int base = lane * R;
+  const M2r M = ld_m2(F.M);
+  M2r MR[5];
+#pragma unroll
+  for (int d = 0; d < 5; ++d) MR[d] = ld_m2(F.MR[d]);
+  const M2r W = ld_m2(F.Winv);
+  // pass 1: zero-start totals of my R chunks
+  double X1 = 0.0, X2 = 0.0;
+  for (int i = 0; i < R; ++i) {
+    const int tl = base + i;
+    const double b1 = tl < T ? st[scan_addr(tl, R)] : 0.0, b2 = tl < T ? st[SS + scan_addr(tl, R)] : 0.0;
+    mv2r(M, X1, X2);
+    X1 += b1;
+    X2 += b2;
+  }
+  // inclusive lane scan (Kogge-Stone, multipliers (M^R)^(2^d))
+  double Y1 = X1, Y2 = X2;
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    const int off = 1 << d;
+    double p1 = __shfl_up_sync(0xffffffffu, Y1, off);
+    double p2 = __shfl_up_sync(0xffffffffu, Y2, off);
+    if (lane >= off) {
+      mv2r(MR[d], p1, p2);
+      Y1 += p1;
+      Y2 += p2;
+    }
+  }
+  // periodic closure: s_{-1} = (I - M^T)^-1 X_{T-1}
+  const int last = (T - 1) / R;
+  double z1 = __shfl_sync(0xffffffffu, Y1, last), z2 = __shfl_sync(0xffffffffu, Y2, last);
+  mv2r(W, z1, z2);
+  // my true carry-in: exclusive zero-start prefix + (M^R)^lane s_{-1}
+  double s1 = __shfl_up_sync(0xffffffffu, Y1, 1), s2 = __shfl_up_sync(0xffffffffu, Y2, 1);
+  if (lane == 0) s1 = s2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 5; ++d)
+    if ((lane >> d) & 1) mv2r(MR[d], z1, z2);
+  s1 += z1;
+  s2 += z2;
+  // pass 2: propagate true states through my chunks
+  for (int i = 0; i < R; ++i) {
+    const int tl = base + i;
+    if (tl < T) {
+      cin[scan_addr(tl, R)] = s1;
+      cin[SS + scan_addr(tl, R)] = s2;
+      mv2r(M, s1, s2);
+      s1 += st[scan_addr(tl, R)];
+      s2 += st[SS + scan_addr(tl, R)];
+    }
+  }
+}
+
 // x <- A^{-1} x for the factorised circulant A = K S^s prod_f F_f (in registers)
 template <int P>
 __device__ void chain_solve(Ctx& c, double (&x)[P]) {
   const StepParams& sp = *c.sp;
   const int T = c.T, t = c.t;
-  double* st = c.scan;
-  double* cin = c.scan + 2 * T;
+  const int R = scan_R(T), SS = scan_stride(T);
+  double* st = c.scan;              // zero-start end states (2 components)
+  double* cin = c.scan + 2 * SS;    // carry-in states
   double* sb = c.bc + 4;
   if (sp.shift != 0) {
     __syncthreads();
@@ -330,13 +410,15 @@ __device__ void chain_solve(Ctx& c, double (&x)[P]) {
       }
     }
   }
+  CL_TR_INIT
+  int nwin = 0;  // windowed factors so far (their end-state buffers alternate)
   for (int f = 0; f < sp.nfac; ++f) {
     const Factor& F = sp.fac[f];
     const bool fwd = F.dir > 0;
     const int tl = fwd ? t : T - 1 - t;
+    double s1 = 0.0, s2 = 0.0;  // zero-start end state of my chunk
     if (c.own) {
       const double a1 = F.a1, a2 = F.a2;
-      double s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int qq = 0; qq < P; ++qq) {
         const int q = fwd ? qq : P - 1 - qq;
@@ -345,26 +427,134 @@ __device__ void chain_solve(Ctx& c, double (&x)[P]) {
         s2 = s1;
         s1 = yv;
       }
-      st[2 * tl] = s1;
-      st[2 * tl + 1] = s2;
+      if (!(T % 32 == 0) && F.win == 0) {
+        st[scan_addr(tl, R)] = s1;
+        st[SS + scan_addr(tl, R)] = s2;
+      }
     }
-    __syncthreads();
-    if (t < 32) lane_scan(F, st, cin, sb, T, t);
-    __syncthreads();
-    if (c.own) {
-      double c1 = cin[2 * tl], c2 = cin[2 * tl + 1];
-      double p1 = sb[0], p2 = sb[1];
+    CL_TR(4)
+    const bool hier = (T % 32 == 0);
+    double c1 = 0.0, c2 = 0.0;
+    if (F.win > 0) {
+      // fast-decaying factor: the true carry of chunk tl is exact to rounding
+      // from the K previous chunks' zero-start end states (Horner), one barrier
+      double* wb = c.scan + 4 * SS + (nwin & 1) * 2 * T;
+      ++nwin;
+      if (c.own) {
+        wb[tl] = s1;
+        wb[T + tl] = s2;
+      }
+      __syncthreads();
+      CL_TR(5)
+      if (c.own) {
+        const M2r M = ld_m2(F.M);
+        const int K = F.win;
 #pragma unroll
-      for (int kb = 0; kb < LOGT; ++kb)
-        if ((tl >> kb) & 1) mv2(F.Mpow[kb], p1, p2);
-      c1 += p1;
-      c2 += p2;
+        for (int k = 16; k >= 1; --k) {
+          if (k <= K) {
+            int u = tl - k;
+            u += u < 0 ? T : 0;
+            mv2r(M, c1, c2);
+            c1 += wb[u];
+            c2 += wb[T + u];
+          }
+        }
+      }
+      CL_TR(7)
+    } else if (hier) {
+      // hierarchical parallel scan over logical chunks (warp-level Kogge-Stone,
+      // then warp 0 over the warp totals with the periodic closure)
+      const int NW = T >> 5, lane = t & 31, w = t >> 5;
+      const int ll = fwd ? lane : 31 - lane;
+      const int lw = fwd ? w : NW - 1 - w;
+      double y1 = s1, y2 = s2;
+#pragma unroll
+      for (int d = 0; d < 5; ++d) {
+        const int off = 1 << d;
+        const int src = (fwd ? lane - off : lane + off) & 31;
+        double p1 = __shfl_sync(0xffffffffu, y1, src), p2 = __shfl_sync(0xffffffffu, y2, src);
+        if (ll >= off) {
+          mv2(F.Mpow[d], p1, p2);
+          y1 += p1;
+          y2 += p2;
+        }
+      }
+      const int s1src = (fwd ? lane - 1 : lane + 1) & 31;
+      double e1 = __shfl_sync(0xffffffffu, y1, s1src), e2 = __shfl_sync(0xffffffffu, y2, s1src);
+      if (ll == 0) e1 = e2 = 0.0;
+      if (ll == 31) {
+        st[lw] = y1;
+        st[32 + lw] = y2;
+      }
+      __syncthreads();
+      CL_TR(5)
+      if (w == 0) {
+        double a1w = lane < NW ? st[lane] : 0.0, a2w = lane < NW ? st[32 + lane] : 0.0;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          const int off = 1 << d;
+          double p1 = __shfl_up_sync(0xffffffffu, a1w, off), p2 = __shfl_up_sync(0xffffffffu, a2w, off);
+          if (lane >= off) {
+            mv2(F.Mpow[5 + d], p1, p2);
+            a1w += p1;
+            a2w += p2;
+          }
+        }
+        double z1 = __shfl_sync(0xffffffffu, a1w, NW - 1), z2 = __shfl_sync(0xffffffffu, a2w, NW - 1);
+        mv2(F.Winv, z1, z2);  // s_{-1}: periodic closure
+        double x1 = __shfl_up_sync(0xffffffffu, a1w, 1), x2 = __shfl_up_sync(0xffffffffu, a2w, 1);
+        if (lane == 0) x1 = x2 = 0.0;
+#pragma unroll
+        for (int d = 0; d < 5; ++d)
+          if ((lane >> d) & 1) mv2(F.Mpow[5 + d], z1, z2);  // (M^32)^lw s_{-1}
+        if (lane < NW) {
+          cin[lane] = x1 + z1;
+          cin[32 + lane] = x2 + z2;
+        }
+      }
+      __syncthreads();
+      CL_TR(6)
+      c1 = cin[lw];
+      c2 = cin[32 + lw];
+#pragma unroll
+      for (int d = 0; d < 5; ++d)
+        if ((ll >> d) & 1) mv2(F.Mpow[d], c1, c2);  // M^ll C_w
+      c1 += e1;
+      c2 += e2;
+      CL_TR(7)
+    } else {
+      __syncthreads();
+      CL_TR(5)
+      if (t < 32) {
+        if (T <= 32)
+          lane_scan_true(F, st, cin, T, t);
+        else
+          lane_scan(F, st, cin, sb, T, t);
+      }
+      CL_TR(6)
+      __syncthreads();
+      CL_TR(7)
+      if (c.own) {
+        c1 = cin[scan_addr(tl, R)];
+        c2 = cin[SS + scan_addr(tl, R)];
+      }
+    }
+    if (c.own) {
+      if (F.win == 0 && !hier && T > 32) {  // add the periodic-closure response M^tl s_{-1}
+        double p1 = sb[0], p2 = sb[1];
+#pragma unroll
+        for (int kb = 0; kb < LOGT; ++kb)
+          if ((tl >> kb) & 1) mv2(F.Mpow[kb], p1, p2);
+        c1 += p1;
+        c2 += p2;
+      }
 #pragma unroll
       for (int qq = 0; qq < P; ++qq) {
         const int q = fwd ? qq : P - 1 - qq;
         x[q] = fma(F.h1[qq], c1, fma(F.h2[qq], c2, x[q]));
       }
     }
+    CL_TR(8)
   }
   if (c.own) {
 #pragma unroll
@@ -403,19 +593,14 @@ __device__ __forceinline__ void vec_store(double* Vi, int t, int T, const double
   }
 }
 
-// (I - phi D) applied to the resident row: contiguous taps (span <= 6) through
-// a register window, else generic taps.  Exact mode, canonical tap order.
-template <int P>
-__device__ __forceinline__ void apply_op2(const Ctx& c, double (&y)[P]) {
-  const StepParams& sp = *c.sp;
-  if (!sp.win2_ok) {
-    stencil_gen<P, false>(c, sp.ntap2, sp.tap2_off, sp.tap2_w, y);
-    return;
-  }
+// Contiguous short stencil (span <= 6, runtime) through a register window of
+// P+6 neighbours: one shared load per point instead of one per tap.
+template <int P, bool EXACT>
+__device__ __forceinline__ void stencil_win_rt(const Ctx& c, int lo, int span, const double* wts,
+                                               double (&y)[P]) {
 #pragma unroll
   for (int q = 0; q < P; ++q) y[q] = 0.0;
   if (!c.own) return;
-  const int lo = sp.win2_lo;
   int tb = c.t + lo / P;
   tb = tb >= c.T ? tb - c.T : tb;
   const int r0 = lo & (P - 1);
@@ -428,15 +613,25 @@ __device__ __forceinline__ void apply_op2(const Ctx& c, double (&y)[P]) {
     tt = tt >= c.T ? tt - c.T : tt;
     win[w] = c.row[(cw & (P - 1)) * c.S + tt];
   }
-  const int span = sp.win2_span;
 #pragma unroll
   for (int k = 0; k <= 6; ++k) {
     if (k <= span) {
-      const double wk = sp.win2_w[k];
+      const double wk = wts[k];
 #pragma unroll
-      for (int q = 0; q < P; ++q) y[q] = fma(wk, win[q + k], y[q]);  // inside GMRES: DFMA
+      for (int q = 0; q < P; ++q) y[q] = madd<EXACT>(y[q], wk, win[q + k]);
     }
   }
+}
+
+// (I - phi D) applied to the resident row inside GMRES (DFMA).
+template <int P>
+__device__ __forceinline__ void apply_op2(const Ctx& c, double (&y)[P]) {
+  const StepParams& sp = *c.sp;
+  if (!sp.win2_ok) {
+    stencil_gen<P, false>(c, sp.ntap2, sp.tap2_off, sp.tap2_w, y);
+    return;
+  }
+  stencil_win_rt<P, false>(c, sp.win2_lo, sp.win2_span, sp.win2_w, y);
 }
 
 constexpr int RS_CAP = 24;  // Hessenberg R kept in shared memory for cap <= RS_CAP
@@ -686,10 +881,17 @@ __device__ __forceinline__ void step_once(Ctx& c, const double (&wd)[SPAN + 1], 
         }
       }
       if (sp.implicit) chain_solve<P>(c, rhs);
+      CL_TR_INIT
       __syncthreads();
       if (c.own) chunk_to_row<P>(c.row, c.t, c.S, rhs);
       __syncthreads();
-      stencil_gen<P, true>(c, sp.ntap, sp.tap_off, sp.tap_w, z[i]);
+      CL_TR(1)
+      if (sp.win1_ok)
+        stencil_win_rt<P, true>(c, sp.win_lo, sp.win_span, sp.win_w, z[i]);
+      else
+        stencil_gen<P, true>(c, sp.ntap, sp.tap_off, sp.tap_w, z[i]);
+      CL_TR(2)
+      CL_TR_STEP
     }
 #pragma unroll
     for (int q = 0; q < P; ++q) y[q] = x[q];
@@ -731,7 +933,7 @@ __global__ void __launch_bounds__(MAXT) relax_kernel(const StepParams* __restric
   c.red = c.row + (size_t)P * c.S;
   c.bc = c.red + 64;
   c.scan = c.bc + 8;
-  c.gm = c.scan + ((KIND == K_SLD || KIND == K_RK) ? 4 * c.T : 0);
+  c.gm = c.scan + ((KIND == K_SLD || KIND == K_RK) ? 4 * scan_stride(c.T) + 4 * c.T : 0);
   c.ws = L.ws ? L.ws + (size_t)blockIdx.x * L.ws_slot : nullptr;
   c.parity = 0;
   c.phase = 0;

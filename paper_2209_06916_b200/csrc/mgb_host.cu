@@ -135,6 +135,7 @@ std::vector<cld> poly_roots(const std::vector<ld>& cr) {
 struct FactorDesc {
   ld a1, a2;
   int dir;
+  ld rho;  // largest |root| of the factor (decay per point of its recurrence)
 };
 
 // Factorise the circulant with stencil (offsets, weights):
@@ -173,12 +174,21 @@ int factorize(const std::vector<long long>& off, const std::vector<double>& w, i
   shift = (int)(lo + (long long)in_r.size());
   auto emit = [&](std::vector<cld>& rs, bool inside) -> int {
     std::vector<bool> used(rs.size(), false);
+    ld pending_real = 0;  // real roots of one direction are merged pairwise into
+    bool have_pending = false;  // one second-order recurrence (fewer scans)
     for (size_t i = 0; i < rs.size(); ++i) {
       if (used[i]) continue;
       used[i] = true;
       const cld mu = inside ? rs[i] : ((ld)1 / rs[i]);
       if (rs[i].imag() == 0) {
-        facs.push_back({mu.real(), 0, inside ? +1 : -1});
+        if (have_pending) {
+          const ld r1 = pending_real, r2 = mu.real();
+          facs.push_back({r1 + r2, -r1 * r2, inside ? +1 : -1, std::max(std::fabs(r1), std::fabs(r2))});
+          have_pending = false;
+        } else {
+          pending_real = mu.real();
+          have_pending = true;
+        }
         continue;
       }
       // find conjugate partner
@@ -195,8 +205,9 @@ int factorize(const std::vector<long long>& off, const std::vector<double>& w, i
       if (best == rs.size() || bd > 1e-8L * std::abs(rs[i]))
         return fail(MGB_ERR_INVALID, "complex root without conjugate partner");
       used[best] = true;
-      facs.push_back({2 * mu.real(), -std::norm(mu), inside ? +1 : -1});
+      facs.push_back({2 * mu.real(), -std::norm(mu), inside ? +1 : -1, std::abs(mu)});
     }
+    if (have_pending) facs.push_back({pending_real, 0, inside ? +1 : -1, std::fabs(pending_real)});
     return MGB_OK;
   };
   int rc = emit(in_r, true);
@@ -229,6 +240,20 @@ void fill_factor_tables(const FactorDesc& fd, int T, int P, Factor& F) {
   F.a1 = (double)fd.a1;
   F.a2 = (double)fd.a2;
   F.dir = fd.dir;
+  // windowed look-back: the carry of chunk t is exact to rounding from the K
+  // previous chunks when (P K + 1) rho^(P K) < 1e-18 (K <= 16, K < T)
+  F.win = 0;
+  if (fd.rho > 0 && fd.rho < 1) {
+    for (int K = 1; K <= 16 && K < T; ++K) {
+      const ld pk = (ld)P * K;
+      if ((pk + 1) * std::pow(fd.rho, pk) < 1e-18L) {
+        F.win = K;
+        break;
+      }
+    }
+  } else if (fd.rho == 0) {
+    F.win = 1;
+  }
   const M2 A{(ld)F.a1, (ld)F.a2, 1, 0};
   M2 Ak = A;
   for (int q = 0; q < P; ++q) {
@@ -450,6 +475,16 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
       for (int j = 0; j < d->stages; ++j) hp.A[i * mgb::MAX_ST + j] = d->rk_a[i * d->stages + j];
     }
     hp.implicit = d->implicit ? 1 : 0;
+    // register-window form of the -cL stencil (contiguous, span <= 6)
+    bool inc = true;
+    for (int k = 1; k < d->n_taps; ++k) inc = inc && off[k] > off[k - 1];
+    const long long sp1 = off.back() - off.front();
+    if (inc && sp1 <= 6 && T >= 8) {
+      hp.win1_ok = 1;
+      hp.win_lo = (int)mod_n(off.front(), n);
+      hp.win_span = (int)sp1;
+      for (int k = 0; k < d->n_taps; ++k) hp.win_w[off[k] - off.front()] = d->weights[k];
+    }
   }
   hp.gain_inv = 1.0;
   if ((dk == mgb::K_RK && hp.implicit) || dk == mgb::K_SLD) {
@@ -498,7 +533,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->exact = (dk == mgb::K_WIN || dk == mgb::K_GEN) ? hp.exact : 1;
   st->threads = ((T + 31) / 32) * 32;
   size_t dbl = (size_t)P * S + 64 + 8;
-  if (dk == mgb::K_RK || dk == mgb::K_SLD) dbl += 4 * (size_t)T;
+  if (dk == mgb::K_RK || dk == mgb::K_SLD) dbl += 4 * (size_t)mgb::scan_stride(T) + 4 * (size_t)T;
   if (dk == mgb::K_SLG) dbl += mgb::GmLayout::total(n);  // Hessenberg state, R, 2 TMA stages
   st->smem = (int)(sizeof(StepParams) + 8 * dbl);
   {

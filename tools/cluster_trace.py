@@ -13,15 +13,20 @@ u = torch.from_numpy(sol.initial_state()).cuda()
 sol.solve(u.clone())
 lib = _native.load()
 buf = (ctypes.c_ulonglong * 16)()
-single = len(sys.argv) > 3 and sys.argv[3] == "single"
-fetch = lib.mgb_trace_fetch_gen if single else lib.mgb_trace_fetch
+mode = sys.argv[3] if len(sys.argv) > 3 else "cluster"
+single = mode == "single"
+fetch = {"single": lib.mgb_trace_fetch_gen if hasattr(lib, "mgb_trace_fetch_gen") else None,
+         "rk": getattr(lib, "mgb_trace_fetch_rk", None)}.get(mode, lib.mgb_trace_fetch)
 fetch(buf)
 orig = sol._timed
 def timed(nm, fn, *a, **k):
     out = fn(*a, **k)
     if nm == target:
         torch.cuda.synchronize(); fetch(buf)
-        if single:
+        if mode == "rk":
+            names = ["", "row write+syncs", "L stencil", "", "factor local pass", "sync1",
+                     "warp-0 carry scan", "sync2", "carry fix-up", "", "", "", "", "", "", ""]
+        elif single:
             names = ["beta", "op2 stencil", "vi load+dot", "block_sum", "axpy+norm dot", "norm sum",
                      "V store+givens", "sync", "backsub+x", "row write+syncs", "", "", "", "", "", ""]
         else:
