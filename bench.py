@@ -221,8 +221,8 @@ def run_gpu(args):
     dom = max(passes.items(), key=lambda kv: kv[1][1])
     roof = None
     fine_cf = passes.get("L0.CF")
-    if fine_cf:
-        bound, work = algorithmic_work(cf, solver, "L0.CF")
+    bound, work = algorithmic_work(cf, solver, "L0.CF") if fine_cf else (None, None)
+    if fine_cf and work:
         per_launch_s = fine_cf[1] / fine_cf[0] / 1e3
         ach = work / per_launch_s / 1e9
         traffic = None
@@ -241,9 +241,9 @@ def run_gpu(args):
                 "share_of_step": round(fine_cf[1] / total_ms, 4)}
     roof_fp64 = None
     fine_fc = passes.get("L0.FC")
-    if fine_fc:
+    _, flops = algorithmic_work(cf, solver, "L0.FC") if fine_fc else (None, None)
+    if fine_fc and flops:
         fp64_peak = fp64_peak_gflops()
-        _, flops = algorithmic_work(cf, solver, "L0.FC")
         ach = flops / (fine_fc[1] / fine_fc[0] / 1e3) / 1e9
         roof_fp64 = {"bound": "fp64", "kernel": "relax_kernel L0.FC (F-relax + C-relax, exact mode)",
                      "achieved": round(ach, 1), "peak": round(fp64_peak, 1), "unit": "GFLOP/s",

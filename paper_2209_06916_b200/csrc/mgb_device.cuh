@@ -1079,6 +1079,183 @@ __global__ void __launch_bounds__(MAXT) relax_kernel(const StepParams* __restric
   }
 }
 
+// ------------------------------------------- explicit-stencil relaxation
+// Dedicated kernel for assembled explicit stencils (the fine ERK levels):
+// stencil weights and geometry live in registers (no shared parameter copy),
+// the resident slice is double-buffered (one CTA barrier per step), outputs
+// are produced in half-chunks straight into the other buffer (fewer live
+// registers -> 3 CTAs/SM), rows stream to HBM with 16-byte stores.  Same
+// argument semantics as relax_kernel (mgb_relax_args).
+template <int P, int SPAN, bool EXACT>
+__device__ __forceinline__ void win_step(const double* __restrict__ src, double* __restrict__ dst,
+                                         int t, int T, int S, int tb, int r0,
+                                         const double (&wd)[SPAN + 1]) {
+  constexpr int H = P >= 8 ? P / 2 : P;  // outputs per pass (window of H + SPAN in registers)
+#pragma unroll
+  for (int h = 0; h < P; h += H) {
+    double win[H + SPAN];
+#pragma unroll
+    for (int w = 0; w < H + SPAN; ++w) {
+      const int cw = r0 + h + w;
+      int tt = tb + cw / P;
+      tt = tt >= T ? tt - T : tt;
+      tt = tt >= T ? tt - T : tt;
+      win[w] = src[(cw & (P - 1)) * S + tt];
+    }
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      // numpy starts from zeros: 0 + w0*v0 == w0*v0 (up to the sign of an exact zero)
+      double acc = EXACT ? __dmul_rn(wd[0], win[q]) : wd[0] * win[q];
+#pragma unroll
+      for (int k = 1; k <= SPAN; ++k) acc = madd<EXACT>(acc, wd[k], win[q + k]);
+      dst[(h + q) * S + t] = acc;
+    }
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void slice_to_global(const double* row, double* dst, int n, int S) {
+  // natural-order 16-byte stores (n even), streaming
+  for (int i = 2 * threadIdx.x; i < n; i += 2 * blockDim.x)
+    __stcs(reinterpret_cast<double2*>(dst + i), make_double2(row[saddr<P>(i, S)], row[saddr<P>(i + 1, S)]));
+}
+
+#ifndef MGB_WIN_MINB
+#define MGB_WIN_MINB 2
+#endif
+// one thread issues an L2 prefetch of a contiguous byte range (no registers, no completion)
+__device__ __forceinline__ void l2_prefetch(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
+
+template <int P, int SPAN, bool EXACT>
+__global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const StepParams* __restrict__ gp,
+                                                                      const RelaxLaunch L) {
+  // Natural-order global traffic: thread t touches elements 2t, 2t+1 (+2*blockDim) with
+  // 16-byte coalesced accesses and scatters/gathers the slice layout in shared memory.
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = gp->n, T = gp->T, S = gp->S;
+  double wd[SPAN + 1];
+#pragma unroll
+  for (int k = 0; k <= SPAN; ++k) wd[k] = gp->win_w[k];
+  const int t = threadIdx.x;
+  const bool own = t < T;
+  const int lo = gp->win_lo;
+  int tb = t + lo / P;
+  tb = tb >= T ? tb - T : tb;
+  const int r0 = lo & (P - 1);
+  double* const row0 = reinterpret_cast<double*>(smem_raw);
+  const int PS = P * S;
+  double* red = row0 + 2 * PS;
+  const mgb_relax_args& a = L.a;
+  const int nthr = blockDim.x;
+  const uint32_t rowbytes = (uint32_t)n * 8u;
+  for (long long k = blockIdx.x; k < a.n_intervals; k += gridDim.x) {
+    const long long kg = a.k_global0 + k;
+    const long long rowbase = k * (long long)a.m;
+    const double* csrc = (kg == 0 && a.c_src0) ? a.c_src0 : (a.c_src ? a.c_src + k * a.c_stride : nullptr);
+    const double* erow = (a.e && kg >= 1) ? a.e + k * a.e_stride : nullptr;
+    __syncthreads();  // previous interval's readers of both buffers are done
+    // interval start: C-point (+ correction, mgrit.py:246) -> slice buffer 0 (and c_out)
+    for (int i = 2 * t; i < n; i += 2 * nthr) {
+      double2 y = csrc ? __ldg(reinterpret_cast<const double2*>(csrc + i)) : make_double2(0.0, 0.0);
+      if (erow) {
+        const double2 ev = __ldg(reinterpret_cast<const double2*>(erow + i));
+        y.x = __dadd_rn(y.x, ev.x);
+        y.y = __dadd_rn(y.y, ev.y);
+      }
+      if (a.c_out) *reinterpret_cast<double2*>(a.c_out + k * a.c_out_stride + i) = y;
+      row0[saddr<P>(i, S)] = y.x;
+      row0[saddr<P>(i + 1, S)] = y.y;
+    }
+    if (t == 0) {  // warm L2 for the next interval this CTA handles
+      const long long kn = k + gridDim.x;
+      if (kn < a.n_intervals) {
+        if (a.c_src) l2_prefetch(a.c_src + kn * a.c_stride, rowbytes);
+        if (a.e) l2_prefetch(a.e + kn * a.e_stride, rowbytes);
+        if (a.tail == 2 && a.cref) l2_prefetch(a.cref + kn * a.cref_stride, rowbytes);
+        if (a.tail == 2 && a.cref_e) l2_prefetch(a.cref_e + kn * a.cref_e_stride, rowbytes);
+      }
+      if (a.g) l2_prefetch(a.g + (rowbase + 1) * n, rowbytes * (uint32_t)(a.n_fsteps + (a.tail ? 1 : 0)));
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int j = 1; j <= a.n_fsteps; ++j) {
+      double* src = row0 + cur * PS;
+      double* dst = row0 + (cur ^ 1) * PS;
+      if (own) win_step<P, SPAN, EXACT>(src, dst, t, T, S, tb, r0, wd);
+      __syncthreads();  // dst complete; src free for step j+1's output
+      if (a.g) {  // upd + g (mgrit.py:142), natural order, then republish
+        const double* gr = a.g + (rowbase + j) * n;
+        for (int i = 2 * t; i < n; i += 2 * nthr) {
+          const double2 gv = __ldg(reinterpret_cast<const double2*>(gr + i));
+          const int s0 = saddr<P>(i, S), s1 = saddr<P>(i + 1, S);
+          dst[s0] = __dadd_rn(dst[s0], gv.x);
+          dst[s1] = __dadd_rn(dst[s1], gv.y);
+        }
+        __syncthreads();
+      }
+      cur ^= 1;
+      if (a.write_f == 2 || (a.write_f == 1 && j == a.n_fsteps))
+        slice_to_global<P>(dst, a.u + (rowbase + j) * n, n, S);
+    }
+    if (a.tail) {  // one more step from the last F-point, into the free buffer
+      const double* src = row0 + cur * PS;
+      double* zb = row0 + (cur ^ 1) * PS;
+      if (own) win_step<P, SPAN, EXACT>(src, zb, t, T, S, tb, r0, wd);
+      __syncthreads();
+      const long long grow = rowbase + a.m;
+      double part = 0.0;
+      for (int i = 2 * t; i < n; i += 2 * nthr) {
+        double2 z = make_double2(zb[saddr<P>(i, S)], zb[saddr<P>(i + 1, S)]);
+        if (a.g) {
+          const double2 gv = __ldg(reinterpret_cast<const double2*>(a.g + grow * n + i));
+          z.x = __dadd_rn(gv.x, z.x);  // g + Phi u (commutative: bitwise either order)
+          z.y = __dadd_rn(gv.y, z.y);
+        }
+        if (a.tail == 1) {  // C-relaxation (mgrit.py:148-149)
+          *reinterpret_cast<double2*>(a.tail_out + k * a.tail_stride + i) = z;
+        } else {  // residual (g + Phi u) - u_C (mgrit.py:159-161)
+          double2 c = __ldg(reinterpret_cast<const double2*>(a.cref + k * a.cref_stride + i));
+          if (a.cref_e) {
+            const double2 ce = __ldg(reinterpret_cast<const double2*>(a.cref_e + k * a.cref_e_stride + i));
+            c.x = __dadd_rn(c.x, ce.x);
+            c.y = __dadd_rn(c.y, ce.y);
+          }
+          const double2 r = make_double2(__dsub_rn(z.x, c.x), __dsub_rn(z.y, c.y));
+          part = fma(r.x, r.x, part);
+          part = fma(r.y, r.y, part);
+          if (a.tail_out) *reinterpret_cast<double2*>(a.tail_out + k * a.tail_stride + i) = r;
+        }
+      }
+      if (a.tail == 2 && a.partials) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        const int w = t >> 5, lane = t & 31;
+        if (lane == 0) red[w] = part;
+        __syncthreads();
+        if (t == 0) {
+          double s = 0.0;
+          for (int i = 0; i < (nthr >> 5); ++i) s += red[i];
+          a.partials[k] = s;
+        }
+      }
+    }
+    if (a.c_last_out && k == a.n_intervals - 1) {  // final C-point (k+1 >= 1)
+      for (int i = 2 * t; i < n; i += 2 * nthr) {
+        double2 v = a.c_src ? __ldg(reinterpret_cast<const double2*>(a.c_src + (k + 1) * a.c_stride + i))
+                            : make_double2(0.0, 0.0);
+        if (a.e) {
+          const double2 ev = __ldg(reinterpret_cast<const double2*>(a.e + (k + 1) * a.e_stride + i));
+          v.x = __dadd_rn(v.x, ev.x);
+          v.y = __dadd_rn(v.y, ev.y);
+        }
+        *reinterpret_cast<double2*>(a.c_last_out + i) = v;
+      }
+    }
+  }
+}
+
 __global__ void sum_kernel(const double* __restrict__ p, long long n, double* out);
 
 }  // namespace mgb

@@ -339,6 +339,7 @@ struct mgb_step {
   StepParams hp;
   StepParams* dp = nullptr;
   int dkind = 0, P = 1, T = 1, S = 1, span = 0, nst = 1, exact = 1;
+  bool vec16 = false;  // relax_win_kernel: 16-byte row accesses
   int threads = 32, smem = 0, max_grid = 1, sms = 148;
   const void* fn = nullptr;
   double* ws = nullptr;
@@ -529,6 +530,8 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->dkind = dk;
   st->P = P; st->T = T; st->S = S;
   st->span = span;
+  const bool win_dedicated = dk == mgb::K_WIN && T <= 256 && span < 16 && n % 2 == 0;
+  st->vec16 = win_dedicated;
   st->nst = dk == mgb::K_RK ? hp.stages : 1;
   st->exact = (dk == mgb::K_WIN || dk == mgb::K_GEN) ? hp.exact : 1;
   st->threads = ((T + 31) / 32) * 32;
@@ -536,10 +539,14 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   if (dk == mgb::K_RK || dk == mgb::K_SLD) dbl += 4 * (size_t)mgb::scan_stride(T) + 4 * (size_t)T;
   if (dk == mgb::K_SLG) dbl += mgb::GmLayout::total(n);  // Hessenberg state, R, 2 TMA stages
   st->smem = (int)(sizeof(StepParams) + 8 * dbl);
+  if (win_dedicated)  // relax_win_kernel: double-buffered slice, weights in registers
+    st->smem = (int)(8 * (2 * (size_t)P * S + 32));  // 2 slices + reduction
   {
     std::lock_guard<std::mutex> lk(reg_mutex());
     auto it = registry().end();
     if (dk == mgb::K_SLG && T <= 256)  // register-rich variant (launch bound 256)
+      it = registry().find(std::make_tuple(dk, P, span, 2, st->exact));
+    if (dk == mgb::K_WIN && !win_dedicated)  // wide slices / long stencils: generic-kernel variant
       it = registry().find(std::make_tuple(dk, P, span, 2, st->exact));
     if (it == registry().end()) it = registry().find(std::make_tuple(dk, P, span, st->nst, st->exact));
     if (it == registry().end()) { delete st; return fail(MGB_ERR_UNSUPPORTED, "no kernel instantiation for this layout"); }
@@ -600,6 +607,14 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   if (a->tail == 1 && !a->tail_out) return fail(MGB_ERR_INVALID, "C-relax tail needs tail_out");
   if (a->tail == 2 && !a->cref) return fail(MGB_ERR_INVALID, "residual tail needs cref");
   if (a->write_f && !a->u) return fail(MGB_ERR_INVALID, "write_f needs u");
+  if (st->vec16) {  // dedicated stencil kernel moves rows with 16-byte accesses
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    const bool ok = al(a->c_src) && al(a->c_src0) && al(a->e) && al(a->c_out) && al(a->c_last_out) &&
+                    al(a->u) && al(a->g) && al(a->tail_out) && al(a->cref) && al(a->cref_e) &&
+                    a->c_stride % 2 == 0 && a->e_stride % 2 == 0 && a->c_out_stride % 2 == 0 &&
+                    a->tail_stride % 2 == 0 && a->cref_stride % 2 == 0 && a->cref_e_stride % 2 == 0;
+    if (!ok) return fail(MGB_ERR_INVALID, "explicit-stencil relax needs 16-byte aligned rows and even strides");
+  }
   mgb::RelaxLaunch L;
   L.a = *a;
   L.ws = nullptr;
