@@ -5,8 +5,8 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v --ex
 SRC := paper_2209_06916_b200/csrc
 OUT := paper_2209_06916_b200/_lib
 BUILD := build/obj
-OBJS := $(BUILD)/mgb_host.o $(BUILD)/k_win_exact.o $(BUILD)/k_win_fast.o $(BUILD)/k_gen.o $(BUILD)/k_rk.o $(BUILD)/k_slgc.o
-HDRS := $(SRC)/mgb_device.cuh $(SRC)/mgb_cluster.cuh $(SRC)/mgb_registry.h include/mgrit_b200.h
+OBJS := $(BUILD)/mgb_host.o $(BUILD)/k_win_exact.o $(BUILD)/k_win_fast.o $(BUILD)/k_gen.o $(BUILD)/k_rk.o $(BUILD)/k_slgc.o $(BUILD)/k_slgc1.o
+HDRS := $(SRC)/mgb_device.cuh $(SRC)/mgb_cluster.cuh $(SRC)/mgb_cluster1.cuh $(SRC)/mgb_registry.h include/mgrit_b200.h
 
 all: $(OUT)/libmgrit_b200.so
 

@@ -1,0 +1,33 @@
+// One-reduction cluster GMRES relaxation instantiations (segment = 32*SEGK points
+// per vector warp, column cap).
+#include "mgb_cluster1.cuh"
+#include "mgb_registry.h"
+
+namespace mgb {
+#define REG_CL1(SEGK, CAP, R, NWMAX)                                                     \
+  register_kernel(KernelKey{K_SLGC1, SEGK, CAP, R, NWMAX},                               \
+                  reinterpret_cast<const void*>(&relax_cl1_kernel<SEGK, CAP, R, NWMAX>))
+// reach R of (I - phi D^(p+1)): p = 1 -> 1 (cap 10), p = 3 -> 2, p = 5 -> 3 (cap 20);
+// NWMAX vector warps per CTA (8: 288 threads, 16: 544 threads with 64-point segments)
+void register_slgc1() {
+  REG_CL1(1, 10, 1, 8);
+  REG_CL1(2, 10, 1, 8);
+  REG_CL1(2, 10, 1, 16);
+  REG_CL1(1, 20, 2, 8);
+  REG_CL1(2, 20, 2, 8);
+  REG_CL1(2, 20, 2, 16);
+  REG_CL1(1, 20, 3, 8);
+  REG_CL1(2, 20, 3, 8);
+  REG_CL1(2, 20, 3, 16);
+}
+}  // namespace mgb
+
+#ifdef MGB_CL_TRACE
+extern "C" int mgb_trace_fetch_c1(unsigned long long* out16) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, mgb::g_cl_trace, 16 * sizeof(unsigned long long));
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(mgb::g_cl_trace, z, sizeof(z));
+  return (int)cudaGetLastError();
+}
+#endif

@@ -47,7 +47,7 @@ constexpr int LOGT = 11;
 constexpr int MAX_CAP = 128;
 constexpr int MAX_WIN = 31;  // register-window stencils: span <= 30
 
-enum { K_WIN = 0, K_GEN = 1, K_RK = 2, K_SLD = 3, K_SLG = 4, K_SLGC = 5 };
+enum { K_WIN = 0, K_GEN = 1, K_RK = 2, K_SLD = 3, K_SLG = 4, K_SLGC = 5, K_SLGC1 = 6 };
 
 // One periodic first/second-order recurrence factor of a factorised
 // circulant (see bandsolve in mgb_host.cu):

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -14,7 +15,7 @@
 #include <tuple>
 #include <vector>
 
-#include "mgb_cluster.cuh"
+#include "mgb_cluster1.cuh"
 #include "mgb_registry.h"
 
 using mgb::Factor;
@@ -53,6 +54,7 @@ void ensure_registered() {
     mgb::register_gen();
     mgb::register_rk();
     mgb::register_slgc();
+    mgb::register_slgc1();
   });
 }
 
@@ -332,6 +334,7 @@ __global__ void sum_kernel(const double* __restrict__ p, long long n, double* ou
 
 struct ClusterVariant {
   int C = 0, P = 0, T = 0, smem = 0, max_clusters = 0;
+  bool one_red = false;  // relax_cl1_kernel (one reduction per Arnoldi step)
   const void* fn = nullptr;
 };
 
@@ -346,13 +349,92 @@ struct mgb_step {
   long long ws_slot = 0;
   int ws_slots = 0;
   std::vector<ClusterVariant> clusters;  // SL_GMRES: cluster sizes 16, 8, 4, 2
+  std::vector<ClusterVariant> clusters1; // SL_GMRES one-reduction variants
 };
 
 namespace {
 // Cluster launch variants for SL_GMRES: C CTAs per interval, P <= 2 points per
 // thread, 32 <= T <= 256 threads per CTA, column cap 10 or 20.
+bool try_cluster_variant(ClusterVariant& v) {
+  if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (v.C > 8 && cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(v.C);
+  cfg.blockDim = dim3(v.T);
+  cfg.dynamicSmemBytes = v.smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = v.C;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, v.fn, &cfg) != cudaSuccess || ncl < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  v.max_clusters = ncl;
+  return true;
+}
+
+// One-reduction variants (relax_cl1_kernel): the (I - phi D) stencil must be the
+// symmetric window -r..r (r <= 3), the SL stencil <= 16 taps; each CTA has
+// NW = nc / (32 SEGK) <= 8 vector warps plus the scalar warp.
+void prepare_clusters1(mgb_step* st) {
+  const StepParams& hp = st->hp;
+  const int n = hp.n, cap = hp.cap;
+  const int capt = cap <= 10 ? 10 : (cap <= 20 ? 20 : 0);
+  if (!capt || !hp.win2_ok || hp.win2_span % 2 || hp.ntap > mgb::C1_MAXSL) return;
+  const int r = hp.win2_span / 2;
+  if (r > mgb::C1_MAXR || hp.win2_lo != (r == 0 ? 0 : n - r)) return;
+  double wmax = 0.0;
+  for (int d = 0; d <= 2 * r; ++d) wmax = std::max(wmax, std::fabs(hp.win2_w[d]));
+  for (int d = 0; d < r; ++d)  // A symmetric (DCGS2 uses u.A V a = a.V^T A u)
+    if (std::fabs(hp.win2_w[d] - hp.win2_w[2 * r - d]) > 1e-12 * wmax) return;
+  for (int C : {16, 8, 4, 2}) {
+    if (n % C) continue;
+    const int nc = n / C;
+    int segk = 0, NW = 0, nwmax = 0;
+    for (int sk : {1, 2}) {
+      if (nc % (32 * sk)) continue;
+      const int nw = nc / (32 * sk);
+      if (nw >= 1 && nw <= 8) { segk = sk; NW = nw; nwmax = 8; break; }
+      if (sk == 2 && nw <= mgb::C1_MAXNW) { segk = sk; NW = nw; nwmax = 16; break; }
+    }
+    if (!segk || 3 * r > nc) continue;
+    const void* fn = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(reg_mutex());
+      auto it = registry().find(std::make_tuple((int)mgb::K_SLGC1, segk, capt, r, nwmax));
+      if (it == registry().end()) continue;
+      fn = it->second;
+    }
+    ClusterVariant v;
+    v.C = C;
+    v.P = segk;
+    v.T = 32 * (NW + 1);
+    v.fn = fn;
+    v.one_red = true;
+    v.smem = (int)mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt);
+    if (v.smem > 227 * 1024) continue;
+    const bool ok = try_cluster_variant(v);
+    if (std::getenv("MGB_DEBUG"))
+      fprintf(stderr, "[mgb] cl1 variant n=%d C=%d segk=%d T=%d smem=%d ok=%d max_clusters=%d\n", n, C, segk,
+              v.T, v.smem, (int)ok, v.max_clusters);
+    if (ok) st->clusters1.push_back(v);
+  }
+}
+
 void prepare_clusters(mgb_step* st) {
   if (st->dkind != mgb::K_SLG) return;
+  prepare_clusters1(st);
   const int n = st->hp.n, cap = st->hp.cap;
   const int capt = cap <= 10 ? 10 : (cap <= 20 ? 20 : 0);
   if (!capt) return;
@@ -621,6 +703,41 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   L.ws_slot = 0;
   long long grid = std::min<long long>(a->n_intervals, st->max_grid);
   static const bool no_cluster = std::getenv("MGB_NO_CLUSTER") != nullptr;
+  static const bool cgs2 = std::getenv("MGB_CL_CGS2") != nullptr;
+  if (st->dkind == mgb::K_SLG && !no_cluster && !cgs2 && !st->clusters1.empty()) {
+    // fewest waves of clusters over the intervals; ties -> larger clusters
+    static const int force_c = std::getenv("MGB_C1_C") ? std::atoi(std::getenv("MGB_C1_C")) : 0;
+    const ClusterVariant* best = nullptr;
+    long long best_w = 0;
+    for (const ClusterVariant& v : st->clusters1) {
+      if (force_c && v.C != force_c) continue;
+      const long long w = (a->n_intervals + v.max_clusters - 1) / v.max_clusters;
+      if (!best || w < best_w) { best = &v; best_w = w; }
+    }
+    static const long long max_waves1 = std::getenv("MGB_C1_WAVES")
+                                            ? std::atoll(std::getenv("MGB_C1_WAVES")) : 2;
+    if (best && best_w <= max_waves1) {
+      const ClusterVariant& v = *best;
+      const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(ncl * v.C));
+      cfg.blockDim = dim3(v.T);
+      cfg.dynamicSmemBytes = v.smem;
+      cfg.stream = (cudaStream_t)stream;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = v.C;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      const StepParams* dpc = st->dp;
+      void* cargs[] = {(void*)&dpc, (void*)&L};
+      CUDA_TRY(cudaLaunchKernelExC(&cfg, v.fn, cargs));
+      g_launches++;
+      return MGB_OK;
+    }
+  }
   if (st->dkind == mgb::K_SLG && !no_cluster) {
     static const long long max_waves = std::getenv("MGB_CLUSTER_WAVES")
                                            ? std::atoll(std::getenv("MGB_CLUSTER_WAVES")) : 2;

@@ -17,6 +17,7 @@ void register_win_fast();
 void register_gen();
 void register_rk();
 void register_slgc();
+void register_slgc1();
 
 // window spans with a compiled register-window variant
 constexpr int kWinSpans[] = {1, 2, 3, 4, 5, 9, 16, 30};

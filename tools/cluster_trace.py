@@ -16,7 +16,8 @@ buf = (ctypes.c_ulonglong * 16)()
 mode = sys.argv[3] if len(sys.argv) > 3 else "cluster"
 single = mode == "single"
 fetch = {"single": lib.mgb_trace_fetch_gen if hasattr(lib, "mgb_trace_fetch_gen") else None,
-         "rk": getattr(lib, "mgb_trace_fetch_rk", None)}.get(mode, lib.mgb_trace_fetch)
+         "rk": getattr(lib, "mgb_trace_fetch_rk", None),
+         "c1": getattr(lib, "mgb_trace_fetch_c1", None)}.get(mode, lib.mgb_trace_fetch)
 fetch(buf)
 orig = sol._timed
 def timed(nm, fn, *a, **k):
@@ -29,6 +30,9 @@ def timed(nm, fn, *a, **k):
         elif single:
             names = ["beta", "op2 stencil", "vi load+dot", "block_sum", "axpy+norm dot", "norm sum",
                      "V store+givens", "sync", "backsub+x", "row write+syncs", "", "", "", "", "", ""]
+        elif mode == "c1":
+            names = ["scalars", "v_j", "Z_j", "u'", "Au'+dots", "syncthreads", "exchange",
+                     "backsub+x", "SL+b dots", "b exchange", "", "", "", "", "", ""]
         else:
           names = ["beta+halo", "passA1", "passB1", "upd1+pub+pd2", "sum2", "corr+upd2+hn",
                  "V/Z+givens", "backsub+x", "SL apply", "row+barrier", "", "", "", "", "gmres total", "steps"]

@@ -52,7 +52,7 @@ __global__ void bench(int iters, int cnt, int mode, double* out, long long* cyc)
 
 int main() {
   double* d; long long* cy; cudaMalloc(&d, 8); cudaMalloc(&cy, 8);
-  for (int C : {8, 16}) for (int T : {128, 256}) for (int mode : {0, 4}) for (int cnt : {1, 21}) {
+  for (int C : {8, 16}) for (int T : {128, 256}) for (int mode : {0, 1, 2, 4}) for (int cnt : {1, 21}) {
     
     auto fn = bench<21>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
