@@ -40,8 +40,7 @@ namespace mgb {
 
 constexpr int C1_MAXR = 3;     // reach of the correction stencil (p <= 5)
 constexpr int C1_MAXNW = 16;   // vector warps per CTA
-constexpr int C1_SLOTS = 48;   // reduction slots per rank: a-part [0,24), b-part [24,48)
-constexpr int C1_HALF = 24;
+constexpr int C1_SLOTS = 24;   // reduction slots per rank (CAP + 3 <= 24)
 constexpr int C1_MAXSL = 16;   // SL taps
 
 struct C1Params {
@@ -72,7 +71,7 @@ struct C1Layout {
     scr = o;    o += NW * 2 * XS;
     cred = o;   o += 2 * C * C1_SLOTS;
     wred = o;   o += NW * C1_SLOTS;
-    Hm = o;     o += (CAP + 1) * CAP + 1;
+    Hm = o;  // (unused)
     R = o;      o += CAP * CAP;
     cs = o;     o += CAP;
     sn = o;     o += CAP;
@@ -147,17 +146,16 @@ __device__ __forceinline__ double c1_A(const double (&w)[2 * R + 1], const doubl
   return s;
 }
 
-// Cluster all-reduce step: the CTA totals of wred slots [0, cnt) (and
-// [C1_HALF, C1_HALF + cnt) if `both`) go to every rank's receive buffer q by
-// st.async, each completing its bytes on that rank's bar[q]; every thread then
-// waits for bar[q]'s phase (C ranks' values plus `extra` bytes of halo points
-// pushed to this CTA during the step).  No cluster barrier: buffer q is
-// rewritten only two reductions later, which needs this CTA's next values.
+// Cluster all-reduce step: the CTA totals of wred slots [0, cnt) go to every
+// rank's receive buffer q by st.async, each completing its bytes on that rank's
+// bar[q]; every thread then waits for bar[q]'s phase (C ranks' values plus
+// `extra` bytes of halo points pushed to this CTA during the step).  No cluster
+// barrier: buffer q is rewritten only two reductions later, which needs this
+// CTA's next values.
 template <int NWMAX>
-__device__ __forceinline__ void c1_exchange(C1Ctx& c, int cnt, bool both, int extra) {
+__device__ __forceinline__ void c1_exchange(C1Ctx& c, int cnt, int extra) {
   const int tid = threadIdx.x;
-  const int idx = tid < C1_HALF ? tid : tid - C1_HALF;
-  if (tid < C1_SLOTS && idx < cnt && (both || tid < C1_HALF)) {
+  if (tid < cnt) {
     double v[NWMAX];
 #pragma unroll
     for (int w = 0; w < NWMAX; ++w) v[w] = w < c.NW ? c.wred[w * C1_SLOTS + tid] : 0.0;
@@ -169,7 +167,7 @@ __device__ __forceinline__ void c1_exchange(C1Ctx& c, int cnt, bool both, int ex
       if (rr < c.C) c1_st_async(cl_map(src, rr), s, cl_map(bsrc, rr));
   }
   if (tid == 0) {
-    const uint32_t bytes = (uint32_t)(8 * c.C * cnt * (both ? 2 : 1) + extra);
+    const uint32_t bytes = (uint32_t)(8 * c.C * cnt + extra);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(c.bar + c.q)),
                  "r"(bytes) : "memory");
   }
@@ -204,40 +202,47 @@ __device__ __forceinline__ double c1_sl(const C1Ctx& c, cg::cluster_group& cl, i
 }
 
 // Transposed partial dots of this warp's segment for reduction R_{j+1}: lane
-// i <= j: V_i.u and V_i.Au, lane j+1: u.u and u.Au (u = vx[3r..], Au = zx[3r..]).
-// No shuffles; rows are read with an odd stride (conflict-free), u/Au broadcast.
+// i <= j: V_i.u, lane j+1: u.u, lane j+2: u.Au (u = vx[3r..], Au = zx[3r..]).
+// No shuffles; rows are read with an odd stride (conflict-free), u broadcast.
 __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
   const int lane = c.lane, S = c.S, off = 3 * c.r;
-  if (lane <= j + 1) {
-    const double* vr = lane <= j ? c.V + c.HW + lane * c.LD + c.seg : c.vx + off;
+  if (lane <= j + 2) {
     const double* uu = c.vx + off;
-    const double* aw = c.zx + off;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+    const double* vr = lane <= j ? c.V + c.HW + lane * c.LD + c.seg : (lane == j + 1 ? uu : c.zx + off);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int e = 0; e < S; e += 4) {
-      const double v0 = vr[e], v1 = vr[e + 1], v2 = vr[e + 2], v3 = vr[e + 3];
-      a0 = fma(v0, uu[e], a0);
-      a1 = fma(v1, uu[e + 1], a1);
-      a2 = fma(v2, uu[e + 2], a2);
-      a3 = fma(v3, uu[e + 3], a3);
-      b0 = fma(v0, aw[e], b0);
-      b1 = fma(v1, aw[e + 1], b1);
-      b2 = fma(v2, aw[e + 2], b2);
-      b3 = fma(v3, aw[e + 3], b3);
+      a0 = fma(vr[e], uu[e], a0);
+      a1 = fma(vr[e + 1], uu[e + 1], a1);
+      a2 = fma(vr[e + 2], uu[e + 2], a2);
+      a3 = fma(vr[e + 3], uu[e + 3], a3);
     }
     c.wred[c.warp * C1_SLOTS + lane] = (a0 + a1) + (a2 + a3);
-    c.wred[c.warp * C1_SLOTS + C1_HALF + lane] = (b0 + b1) + (b2 + b3);
   }
 }
 
 // One corrected SL coarse step: b = SL(in_row) then x = GMRES(I - phi D, b) on
 // this CTA's own points (x[k] = point seg + lane + 32 k of the vector warps).
+//
+// Arnoldi with one reduction per step.  Reduction R_j carries, for the
+// candidate u_j (first Gram-Schmidt pass done, second pending):
+//   a = V_{<j}^T u_j,  nu = u_j.u_j,  c = u_j.A u_j                 (j + 2 values)
+// Step j then forms (scalar warp, broadcast through shared memory):
+//   hn = sqrt(nu - |a|^2) = H[j][j-1];   column j-1 of H = h1 + a  (second pass)
+//   v_j = (u_j - V a) / hn                                          (re-orthogonalised)
+// and the first pass of the next column.  A = I - phi D is symmetric, so the
+// Arnoldi relation A V = V H gives V^T A v_j = hn e_{j-1} (three-term, Lanczos)
+// and v_j.A v_j = c / hn^2 - 2 a_{j-1} (up to O(eps^2)):
+//   h1' = hn e_{j-1} + hj e_j,   u_{j+1} = A v_j - hn v_{j-1} - hj v_j.
+// Whatever the first pass leaves in span(V) is O(eps) and is removed by the
+// full second pass one step later, so H and the basis agree with the
+// reference's MGS GMRES (circulant.py:262-332) to rounding.
 template <int SEGK, int CAP, int R, int NWMAX>
 __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int& depth_out,
                         double& res_out) {
   const C1Params& P = *c.p;
   constexpr int KX = SEGK + 1;  // lane iterations over a segment +- 3r (6r <= 18 < 32)
   constexpr int r = R;
-  static_assert(CAP + 2 <= C1_HALF, "reduction slots");
+  static_assert(CAP + 3 <= C1_SLOTS, "reduction slots");
   const int LD = c.LD, S = c.S, lane = c.lane;
   double w2[2 * R + 1];
 #pragma unroll
@@ -272,31 +277,26 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       c.zx[xx] = c1_A<R>(w2, c.vx, xx);
     }
     __syncwarp();
-    c1_dots(c, -1);  // lane 0: b.b and b.Ab
+    c1_dots(c, -1);  // lane 0: b.b, lane 1: b.Ab
   }
   CL_TR(8)
   __syncthreads();
-  c1_exchange<NWMAX>(c, 1, true, 0);  // also: every CTA finished its SL reads of in_row
+  c1_exchange<NWMAX>(c, 2, 0);  // also: every CTA finished its SL reads of in_row
   CL_TR(9)
 
-  double h1 = 0.0;    // scalar warp, lane i: first-pass coefficient h1_i of the pending column
+  // scalar warp state: lane i holds h1_i (first-pass coefficient of the pending column)
+  double h1 = 0.0;
   double beta = 0.0, ibeta = 0.0;
-  double* coef = c.hc + CAP + 2;  // [2i] = a_i, [2i+1] = h1'_i (i < j); then inv, h1'_j, flags
+  double* coef = c.hc + CAP + 2;  // [i] = a_i (i < j); [CAP..]: inv, hj, hn, flags
   int j = 0;
   for (;; ++j) {
     // ---- scalars of step j, once per CTA (scalar warp); broadcast through smem
-    double ai = 0.0, hp = 0.0, hn = 0.0, nu = 0.0;
+    double ai = 0.0, hn = 0.0;
     if (!c.vec) {
-      double aa = 0.0, bb = 0.0;
-      if (lane <= j) {
-        aa = c1_total(c, c.q, lane);
-        bb = c1_total(c, c.q, C1_HALF + lane);
-      }
-      nu = __shfl_sync(0xffffffffu, aa, j);
-      const double cc = __shfl_sync(0xffffffffu, bb, j);
-      ai = lane < j ? aa : 0.0;
-      const double bi = lane < j ? bb : 0.0;
-      // |a|^2 = O(eps^2) nu unless the first pass failed (then: explicit norm below)
+      const double tot = lane <= j + 1 ? c1_total(c, c.q, lane) : 0.0;
+      const double nu = __shfl_sync(0xffffffffu, tot, j);
+      const double cc = __shfl_sync(0xffffffffu, tot, (j + 1) & 31);
+      ai = lane < j ? tot : 0.0;
       const double na2 = c1_wsum(ai * ai);
       const double hn2 = nu - na2;
       hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
@@ -305,33 +305,27 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
         ibeta = beta > 0.0 ? 1.0 / beta : 0.0;
       }
       const double inv = hn > 0.0 ? 1.0 / hn : 1.0;
-      // first-pass coefficients of the next column: h1' = V^T A v_j = (b - M a) / hn and
-      // h1'_j = (c - 2 a.b + a.M a) / hn^2.  a = O(eps) after the first pass, so the
-      // M a / a.b terms are O(eps) and are left to the delayed second pass, which
-      // re-orthogonalises u_{j+1} against [V v_j] one step later (H column = h1' + a').
-      if (lane < j) hp = bi * inv;
-      if (lane == j) hp = cc * (inv * inv);
-      if (lane < j) {
-        coef[2 * lane] = ai;
-        coef[2 * lane + 1] = hp;
-      }
-      if (lane == j) coef[2 * CAP + 1] = hp;
+      const double alast = __shfl_sync(0xffffffffu, ai, (j + 31) & 31);
+      if (lane < j) coef[lane] = ai;
       if (lane == 0) {
-        coef[2 * CAP] = inv;
-        coef[2 * CAP + 2] = (j > 0 && !(hn2 >= 0.5 * nu)) ? 1.0 : 0.0;  // cancelling update
-        coef[2 * CAP + 3] = beta == 0.0 ? 1.0 : 0.0;                     // zero right-hand side
+        coef[CAP] = inv;
+        coef[CAP + 1] = cc * (inv * inv) - (j > 0 ? 2.0 * alast : 0.0);  // hj = v_j.A v_j
+        coef[CAP + 2] = j > 0 ? hn : 0.0;
+        coef[CAP + 3] = (j > 0 && !(hn2 >= 0.5 * nu)) ? 1.0 : 0.0;  // cancelling update
+        coef[CAP + 4] = beta == 0.0 ? 1.0 : 0.0;                    // zero right-hand side
+        coef[CAP + 5] = cc;
       }
     }
     c.q ^= 1;
     __syncthreads();
-    if (coef[2 * CAP + 3] != 0.0) {  // zero right-hand side (circulant.py:274-278), uniform
+    if (coef[CAP + 4] != 0.0) {  // zero right-hand side (circulant.py:274-278), uniform
 #pragma unroll
       for (int k = 0; k < SEGK; ++k) x[k] = 0.0;
       depth_out = 0;
       res_out = 0.0;
       return;
     }
-    if (coef[2 * CAP + 2] != 0.0) {
+    if (coef[CAP + 3] != 0.0) {
       // cancelling Pythagorean update: explicit ||u_j - V a||^2 (uniform branch)
       if (c.vec) {
         const double* Uh = c.U + pu * LD + c.HW;
@@ -339,7 +333,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
 #pragma unroll
         for (int k = 0; k < SEGK; ++k) w[k] = Uh[c.seg + lane + 32 * k];
         for (int i = 0; i < j; ++i) {
-          const double a_b = coef[2 * i];
+          const double a_b = coef[i];
 #pragma unroll
           for (int k = 0; k < SEGK; ++k) w[k] = fma(-a_b, Vh[i * LD + c.seg + lane + 32 * k], w[k]);
         }
@@ -350,18 +344,17 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
         if (lane == 0) c.wred[c.warp * C1_SLOTS] = s;
       }
       __syncthreads();
-      c1_exchange<NWMAX>(c, 1, false, 0);
+      c1_exchange<NWMAX>(c, 1, 0);
       if (!c.vec) {  // redo the hn-dependent scalars
         const double hn2 = c1_total(c, c.q, 0);
-        const double hn_old = hn;
         hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
         const double inv = hn > 0.0 ? 1.0 / hn : 1.0;
-        const double sc = hn > 0.0 ? hn_old / hn : 1.0;  // h1' = (b - M a) / hn
-        if (lane < j) hp *= sc;
-        if (lane == j) hp *= sc * sc;
-        if (lane < j) coef[2 * lane + 1] = hp;
-        if (lane == j) coef[2 * CAP + 1] = hp;
-        if (lane == 0) coef[2 * CAP] = inv;
+        const double alast = __shfl_sync(0xffffffffu, ai, (j + 31) & 31);
+        if (lane == 0) {
+          coef[CAP] = inv;
+          coef[CAP + 1] = coef[CAP + 5] * (inv * inv) - 2.0 * alast;
+          coef[CAP + 2] = hn;
+        }
       }
       c.q ^= 1;
       __syncthreads();
@@ -369,18 +362,11 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
     CL_TR(0)
 
     if (!c.vec) {
-      // ---- scalar warp: finalise column j-1 and its Givens rotation
+      // ---- scalar warp: finalise column j-1 (h1 + a, hn) and its Givens rotation
       if (j > 0) {
         const int jc = j - 1;
-        if (lane < j) {
-          const double h = h1 + ai;
-          c.Hm[jc * (CAP + 1) + lane] = h;
-          c.hc[lane] = h;
-        }
-        if (lane == 0) {
-          c.Hm[jc * (CAP + 1) + j] = hn;
-          c.hc[j] = hn;
-        }
+        if (lane < j) c.hc[lane] = h1 + ai;
+        if (lane == 0) c.hc[j] = hn;
         __syncwarp();
         if (lane == 0) {
           double hi = c.hc[0];
@@ -408,35 +394,33 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
         c.flg[0] = 0.0;
         c.flg[1] = 1.0;
       }
+      // first-pass coefficients of column j: h1' = hn e_{j-1} + hj e_j
+      const double hj = coef[CAP + 1];
+      h1 = lane == j ? hj : (lane + 1 == j ? hn : 0.0);
     } else if (j < P.cap) {
-      // ---- vector warps: v_j, A v_j, u_{j+1}, A u_{j+1}, partial dots of R_{j+1}
+      // ---- vector warps: v_j, u_{j+1} = A v_j - hn v_{j-1} - hj v_j, A u_{j+1}, dots
       const double* Uh = c.U + pu * LD + c.HW;
       double* Un = c.U + (pu ^ 1) * LD + c.HW;
-      const double inv = coef[2 * CAP];
-      // one pass over the basis: v = u_j - V a (segment +- 3r), sh = V h1'
-      double v[KX], sh[KX];
+      const double inv = coef[CAP];
+      double v[KX];
 #pragma unroll
       for (int k = 0; k < KX; ++k) {
         const int xx = lane + 32 * k;
         v[k] = xx < XE ? Uh[e0 + xx] : 0.0;
-        sh[k] = 0.0;
       }
-      const double2* cf2 = reinterpret_cast<const double2*>(coef);
 #pragma unroll
       for (int i0 = 0; i0 < CAP; i0 += 4) {
         if (i0 < j) {
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
             const int i = i0 + ii;
-            double2 ah = cf2[i];
-            if (i >= j) ah = make_double2(0.0, 0.0);
+            const double a_b = i < j ? coef[i] : 0.0;
             const double* Vi = Vh + i * LD + e0;
 #pragma unroll
             for (int k = 0; k < KX; ++k) {
               const int xx = lane + 32 * k;
               const double vi = (i < j && xx < XE) ? Vi[xx] : 0.0;
-              v[k] = fma(-ah.x, vi, v[k]);
-              sh[k] = fma(ah.y, vi, sh[k]);
+              v[k] = fma(-a_b, vi, v[k]);
             }
           }
         }
@@ -453,15 +437,18 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       }
       CL_TR(1)
       __syncwarp();
-      // u_{j+1} = A v_j - V h1' - v_j h1'_j on the segment +- r
       double u[KX];
       {
-        const double h_b = coef[2 * CAP + 1];
+        const double hj = coef[CAP + 1], hb = coef[CAP + 2];
+        const double* Vp = Vh + (j > 0 ? j - 1 : 0) * LD + e0;
 #pragma unroll
         for (int k = 0; k < KX; ++k) {
           const int xx = lane + 32 * k;
           u[k] = 0.0;
-          if (xx >= 2 * r && xx < XE - 2 * r) u[k] = fma(-h_b, v[k], c1_A<R>(w2, c.vx, xx) - sh[k]);
+          if (xx >= 2 * r && xx < XE - 2 * r) {
+            const double vp = j > 0 ? Vp[xx] : 0.0;
+            u[k] = fma(-hj, v[k], fma(-hb, vp, c1_A<R>(w2, c.vx, xx)));
+          }
         }
       }
       CL_TR(2)
@@ -511,10 +498,9 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       }
       break;
     }
-    c1_exchange<NWMAX>(c, j + 2, true, 8 * 6 * r);
+    c1_exchange<NWMAX>(c, j + 3, 8 * 6 * r);
     CL_TR(6)
     CL_TR_STEP
-    h1 = hp;
     pu ^= 1;
   }
   // ---- back substitution R y = g (scalar warp), x = V y on the own points
