@@ -9,7 +9,13 @@ namespace mgb {
                   reinterpret_cast<const void*>(&relax_cl1_kernel<SEGK, CAP, R, NWMAX>))
 // reach R of (I - phi D^(p+1)): p = 1 -> 1 (cap 10), p = 3 -> 2, p = 5 -> 3 (cap 20);
 // NWMAX vector warps per CTA (8: 288 threads, 16: 544 threads with 64-point segments)
+#define REG_CL1B(SEGK, CAP, R)                                                           \
+  register_kernel(KernelKey{K_SLGC1, SEGK, CAP, R, 108},                                 \
+                  reinterpret_cast<const void*>(&relax_cl1_kernel<SEGK, CAP, R, 8, 2>))
 void register_slgc1() {
+  // two CTAs per SM (<= 112 registers): single-wave launches of mid-sized levels
+  REG_CL1B(2, 20, 2);
+  REG_CL1B(2, 20, 3);
   REG_CL1(1, 10, 1, 8);
   REG_CL1(2, 10, 1, 8);
   REG_CL1(2, 10, 1, 16);

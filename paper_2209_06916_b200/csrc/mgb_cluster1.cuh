@@ -566,8 +566,8 @@ __device__ __forceinline__ double c1_sum_to_rank0(C1Ctx& c, double v) {
 
 // Interval relaxation with corrected SL steps, one cluster per interval, same
 // argument semantics as relax_kernel / relax_cluster_kernel (mgb_relax_args).
-template <int SEGK, int CAP, int R, int NWMAX>
-__global__ void __launch_bounds__(32 * (NWMAX + 1), 1)
+template <int SEGK, int CAP, int R, int NWMAX, int MINB = 1>
+__global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
     relax_cl1_kernel(const StepParams* __restrict__ gp, const RelaxLaunch L) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -335,6 +335,7 @@ __global__ void sum_kernel(const double* __restrict__ p, long long n, double* ou
 struct ClusterVariant {
   int C = 0, P = 0, T = 0, smem = 0, max_clusters = 0;
   bool one_red = false;  // relax_cl1_kernel (one reduction per Arnoldi step)
+  int occ = 1;           // CTAs per SM the variant is compiled for
   const void* fn = nullptr;
 };
 
@@ -409,10 +410,12 @@ void prepare_clusters1(mgb_step* st) {
       if (sk == 2 && nw <= mgb::C1_MAXNW) { segk = sk; NW = nw; nwmax = 16; break; }
     }
     if (!segk || 3 * r > nc) continue;
+    for (int occ2 = 0; occ2 < 2; ++occ2) {
+    if (occ2 && !(nwmax == 8 && segk == 2 && capt == 20 && r >= 2)) continue;
     const void* fn = nullptr;
     {
       std::lock_guard<std::mutex> lk(reg_mutex());
-      auto it = registry().find(std::make_tuple((int)mgb::K_SLGC1, segk, capt, r, nwmax));
+      auto it = registry().find(std::make_tuple((int)mgb::K_SLGC1, segk, capt, r, occ2 ? 108 : nwmax));
       if (it == registry().end()) continue;
       fn = it->second;
     }
@@ -422,13 +425,15 @@ void prepare_clusters1(mgb_step* st) {
     v.T = 32 * (NW + 1);
     v.fn = fn;
     v.one_red = true;
+    v.occ = occ2 ? 2 : 1;
     v.smem = (int)mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt);
     if (v.smem > 227 * 1024) continue;
     const bool ok = try_cluster_variant(v);
     if (std::getenv("MGB_DEBUG"))
-      fprintf(stderr, "[mgb] cl1 variant n=%d C=%d segk=%d T=%d smem=%d ok=%d max_clusters=%d\n", n, C, segk,
-              v.T, v.smem, (int)ok, v.max_clusters);
+      fprintf(stderr, "[mgb] cl1 variant n=%d C=%d segk=%d T=%d occ2=%d smem=%d ok=%d max_clusters=%d\n", n, C,
+              segk, v.T, occ2, v.smem, (int)ok, v.max_clusters);
     if (ok) st->clusters1.push_back(v);
+    }
   }
 }
 
@@ -711,6 +716,8 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
     long long best_w = 0;
     for (const ClusterVariant& v : st->clusters1) {
       if (force_c && v.C != force_c) continue;
+      static const bool no_occ2 = std::getenv("MGB_C1_NO_OCC2") != nullptr;
+      if (no_occ2 && v.occ == 2) continue;
       const long long w = (a->n_intervals + v.max_clusters - 1) / v.max_clusters;
       if (!best || w < best_w) { best = &v; best_w = w; }
     }
