@@ -290,13 +290,19 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
   double* coef = c.hc + CAP + 2;  // [i] = a_i (i < j); [CAP..]: inv, hj, hn, flags
   int j = 0;
   for (;; ++j) {
-    // ---- scalars of step j, once per CTA (scalar warp); broadcast through smem
-    double ai = 0.0, hn = 0.0;
+    // ---- step j.  Scalar warp: a_i -> smem, named barrier 1 (arrive only); then
+    // |a|^2, hn, 1/hn, hj -> smem, named barrier 2.  Vector warps run the
+    // re-orthogonalisation pass u_j - V a between the two barriers.
+    double ai = 0.0, hn = 0.0, nu = 0.0;
+    const uint32_t nthr = blockDim.x;
     if (!c.vec) {
       const double tot = lane <= j + 1 ? c1_total(c, c.q, lane) : 0.0;
-      const double nu = __shfl_sync(0xffffffffu, tot, j);
-      const double cc = __shfl_sync(0xffffffffu, tot, (j + 1) & 31);
       ai = lane < j ? tot : 0.0;
+      if (lane < j) coef[lane] = ai;
+      __threadfence_block();
+      asm volatile("bar.arrive 1, %0;" ::"r"(nthr) : "memory");
+      nu = __shfl_sync(0xffffffffu, tot, j);
+      const double cc = __shfl_sync(0xffffffffu, tot, (j + 1) & 31);
       const double na2 = c1_wsum(ai * ai);
       const double hn2 = nu - na2;
       hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
@@ -306,7 +312,6 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       }
       const double inv = hn > 0.0 ? 1.0 / hn : 1.0;
       const double alast = __shfl_sync(0xffffffffu, ai, (j + 31) & 31);
-      if (lane < j) coef[lane] = ai;
       if (lane == 0) {
         coef[CAP] = inv;
         coef[CAP + 1] = cc * (inv * inv) - (j > 0 ? 2.0 * alast : 0.0);  // hj = v_j.A v_j
@@ -315,9 +320,40 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
         coef[CAP + 4] = beta == 0.0 ? 1.0 : 0.0;                    // zero right-hand side
         coef[CAP + 5] = cc;
       }
+      __threadfence_block();
+      asm volatile("bar.arrive 2, %0;" ::"r"(nthr) : "memory");
     }
     c.q ^= 1;
-    __syncthreads();
+    const double* Uh = c.U + pu * LD + c.HW;
+    double v[KX];  // vector warps: u_j - V a on the segment +- 3r
+    if (c.vec) {
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+      if (j < P.cap) {
+#pragma unroll
+        for (int k = 0; k < KX; ++k) {
+          const int xx = lane + 32 * k;
+          v[k] = xx < XE ? Uh[e0 + xx] : 0.0;
+        }
+#pragma unroll
+        for (int i0 = 0; i0 < CAP; i0 += 4) {
+          if (i0 < j) {
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) {
+              const int i = i0 + ii;
+              const double a_b = i < j ? coef[i] : 0.0;
+              const double* Vi = Vh + i * LD + e0;
+#pragma unroll
+              for (int k = 0; k < KX; ++k) {
+                const int xx = lane + 32 * k;
+                const double vi = (i < j && xx < XE) ? Vi[xx] : 0.0;
+                v[k] = fma(-a_b, vi, v[k]);
+              }
+            }
+          }
+        }
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(nthr) : "memory");
+    }
     if (coef[CAP + 4] != 0.0) {  // zero right-hand side (circulant.py:274-278), uniform
 #pragma unroll
       for (int k = 0; k < SEGK; ++k) x[k] = 0.0;
@@ -328,18 +364,12 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
     if (coef[CAP + 3] != 0.0) {
       // cancelling Pythagorean update: explicit ||u_j - V a||^2 (uniform branch)
       if (c.vec) {
-        const double* Uh = c.U + pu * LD + c.HW;
-        double w[SEGK];
-#pragma unroll
-        for (int k = 0; k < SEGK; ++k) w[k] = Uh[c.seg + lane + 32 * k];
-        for (int i = 0; i < j; ++i) {
-          const double a_b = coef[i];
-#pragma unroll
-          for (int k = 0; k < SEGK; ++k) w[k] = fma(-a_b, Vh[i * LD + c.seg + lane + 32 * k], w[k]);
-        }
         double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < SEGK; ++k) s = fma(w[k], w[k], s);
+        for (int k = 0; k < KX; ++k) {
+          const int xx = lane + 32 * k;
+          if (xx >= 3 * r && xx < 3 * r + S) s = fma(v[k], v[k], s);
+        }
         s = c1_wsum(s);
         if (lane == 0) c.wred[c.warp * C1_SLOTS] = s;
       }
@@ -399,32 +429,8 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       h1 = lane == j ? hj : (lane + 1 == j ? hn : 0.0);
     } else if (j < P.cap) {
       // ---- vector warps: v_j, u_{j+1} = A v_j - hn v_{j-1} - hj v_j, A u_{j+1}, dots
-      const double* Uh = c.U + pu * LD + c.HW;
       double* Un = c.U + (pu ^ 1) * LD + c.HW;
       const double inv = coef[CAP];
-      double v[KX];
-#pragma unroll
-      for (int k = 0; k < KX; ++k) {
-        const int xx = lane + 32 * k;
-        v[k] = xx < XE ? Uh[e0 + xx] : 0.0;
-      }
-#pragma unroll
-      for (int i0 = 0; i0 < CAP; i0 += 4) {
-        if (i0 < j) {
-#pragma unroll
-          for (int ii = 0; ii < 4; ++ii) {
-            const int i = i0 + ii;
-            const double a_b = i < j ? coef[i] : 0.0;
-            const double* Vi = Vh + i * LD + e0;
-#pragma unroll
-            for (int k = 0; k < KX; ++k) {
-              const int xx = lane + 32 * k;
-              const double vi = (i < j && xx < XE) ? Vi[xx] : 0.0;
-              v[k] = fma(-a_b, vi, v[k]);
-            }
-          }
-        }
-      }
       double* Vj = Vh + j * LD;
 #pragma unroll
       for (int k = 0; k < KX; ++k) {
