@@ -16,6 +16,16 @@ void register_slgc1() {
   // two CTAs per SM (<= 112 registers): single-wave launches of mid-sized levels
   REG_CL1B(2, 20, 2);
   REG_CL1B(2, 20, 3);
+  // wide segments (cluster sizes 1-4 on long rows): lane-parallel dots, L2 overflow rows
+  REG_CL1(4, 20, 2, 16);
+  REG_CL1(8, 20, 2, 8);
+  REG_CL1(8, 20, 2, 16);
+  REG_CL1(4, 20, 3, 16);
+  REG_CL1(8, 20, 3, 8);
+  REG_CL1(8, 20, 3, 16);
+  REG_CL1(4, 10, 1, 16);
+  REG_CL1(8, 10, 1, 8);
+  REG_CL1(8, 10, 1, 16);
   REG_CL1(1, 10, 1, 8);
   REG_CL1(2, 10, 1, 8);
   REG_CL1(2, 10, 1, 16);

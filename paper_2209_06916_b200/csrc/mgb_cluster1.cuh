@@ -44,12 +44,11 @@ constexpr int C1_SLOTS = 24;   // reduction slots per rank (CAP + 3 <= 24)
 constexpr int C1_MAXSL = 16;   // SL taps
 
 struct C1Params {
-  int n, nc, C, NW, S, r, HW, LD, ntap, cap;
+  int n, nc, C, NW, S, r, HW, LD, ntap, cap, K, pad0_;
   double tol;
   int tap_off[C1_MAXSL];
   double tap_w[C1_MAXSL];
   double w2[2 * C1_MAXR + 1];
-  double pad_;
 };
 static_assert(sizeof(C1Params) % 16 == 0, "C1Params must be 16-byte sized");
 
@@ -61,11 +60,11 @@ __host__ __device__ inline int c1_ld(int nc, int r) { return nc + 6 * r + 1; }
 // the first GMRES reduction, and U[1] is first written after it.
 struct C1Layout {
   int V, U, in_row, scr, cred, wred, Hm, R, cs, sn, gg, ybuf, hc, flg, total;
-  __host__ __device__ C1Layout(int nc, int NW, int S, int r, int C, int CAP) {
+  __host__ __device__ C1Layout(int nc, int NW, int S, int r, int C, int CAP, int K) {
     const int LD = c1_ld(nc, r);
     const int XS = S + 6 * r + 2;
     int o = 0;
-    V = o;      o += CAP * LD;
+    V = o;      o += (K < CAP ? K : CAP) * LD;
     U = o;      o += 2 * LD;
     in_row = U + LD + 3 * r;
     scr = o;    o += NW * 2 * XS;
@@ -84,8 +83,10 @@ struct C1Layout {
   }
 };
 
-__host__ __device__ inline size_t c1_smem_bytes(int nc, int NW, int S, int r, int C, int CAP) {
-  return sizeof(C1Params) + 8 * (size_t)C1Layout(nc, NW, S, r, C, CAP).total;
+// K = basis vectors resident in shared memory; V_K .. V_{CAP-1} live in the
+// CTA's L2-resident workspace slot (same halo'd row layout)
+__host__ __device__ inline size_t c1_smem_bytes(int nc, int NW, int S, int r, int C, int CAP, int K) {
+  return sizeof(C1Params) + 8 * (size_t)C1Layout(nc, NW, S, r, C, CAP, K).total;
 }
 
 // fixed-order warp sums, broadcast from lane 0 (bitwise identical in every lane)
@@ -116,7 +117,8 @@ __device__ __forceinline__ double c1_tree(double (&v)[N]) {
 
 struct C1Ctx {
   const C1Params* p;
-  double *V, *U, *in_row, *vx, *zx, *cred, *wred, *Hm, *R, *cs, *sn, *gg, *ybuf, *hc, *flg;
+  double *V, *Vg, *U, *in_row, *vx, *zx, *cred, *wred, *Hm, *R, *cs, *sn, *gg, *ybuf, *hc, *flg;
+  int K;  // basis rows resident in shared memory
   uint64_t* bar;  // bar[q]: transaction barrier of receive buffer q
   int lane, warp, NW, C, rank, S, seg, r, HW, LD, nc, n, base, q, ph;
   bool vec;
@@ -144,6 +146,14 @@ __device__ __forceinline__ double c1_A(const double (&w)[2 * R + 1], const doubl
 #pragma unroll
   for (int d = 0; d <= 2 * R; ++d) s = __dadd_rn(s, __dmul_rn(w[d], src[x - R + d]));
   return s;
+}
+
+// halo'd basis row i: shared memory for i < K, else the CTA's workspace slot
+// (OVF = false: every row is resident, plain shared-memory addressing)
+template <bool OVF>
+__device__ __forceinline__ double* c1_row(const C1Ctx& c, int i) {
+  if constexpr (!OVF) return c.V + (size_t)i * c.LD + c.HW;
+  return (i < c.K ? c.V + (size_t)i * c.LD : c.Vg + (size_t)(i - c.K) * c.LD) + c.HW;
 }
 
 // Cluster all-reduce step: the CTA totals of wred slots [0, cnt) go to every
@@ -208,7 +218,7 @@ __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
   const int lane = c.lane, S = c.S, off = 3 * c.r;
   if (lane <= j + 2) {
     const double* uu = c.vx + off;
-    const double* vr = lane <= j ? c.V + c.HW + lane * c.LD + c.seg : (lane == j + 1 ? uu : c.zx + off);
+    const double* vr = lane <= j ? c1_row<false>(c, lane) + c.seg : (lane == j + 1 ? uu : c.zx + off);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int e = 0; e < S; e += 4) {
       a0 = fma(vr[e], uu[e], a0);
@@ -217,6 +227,48 @@ __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
       a3 = fma(vr[e + 3], uu[e + 3], a3);
     }
     c.wred[c.warp * C1_SLOTS + lane] = (a0 + a1) + (a2 + a3);
+  }
+}
+
+// Wide segments (SEGK >= 4): lane-parallel products over the lane's own points,
+// then fixed-order warp butterflies, four rows interleaved.  Rows as c1_dots.
+template <int SEGK>
+__device__ __forceinline__ void c1_dots_lanes(C1Ctx& c, int j) {
+  const int lane = c.lane, off = 3 * c.r;
+  double uo[SEGK], ao[SEGK];
+#pragma unroll
+  for (int k = 0; k < SEGK; ++k) {
+    uo[k] = c.vx[off + lane + 32 * k];
+    ao[k] = c.zx[off + lane + 32 * k];
+  }
+  for (int i0 = 0; i0 <= j + 2; i0 += 4) {
+    double p[4];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int i = i0 + ii;
+      double s = 0.0;
+      if (i <= j) {
+        const double* vr = c1_row<(SEGK >= 4)>(c, i) + c.seg + lane;
+#pragma unroll
+        for (int k = 0; k < SEGK; ++k) s = fma(vr[32 * k], uo[k], s);
+      } else if (i == j + 1) {
+#pragma unroll
+        for (int k = 0; k < SEGK; ++k) s = fma(uo[k], uo[k], s);
+      } else if (i == j + 2) {
+#pragma unroll
+        for (int k = 0; k < SEGK; ++k) s = fma(ao[k], uo[k], s);
+      }
+      p[ii] = s;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) p[ii] += __shfl_xor_sync(0xffffffffu, p[ii], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+        if (i0 + ii <= j + 2) c.wred[c.warp * C1_SLOTS + i0 + ii] = p[ii];
+    }
   }
 }
 
@@ -249,7 +301,6 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
   for (int d = 0; d <= 2 * R; ++d) w2[d] = P.w2[d];
   const int XE = S + 6 * r;     // extended segment length
   const int e0 = c.seg - 3 * r; // local index of scratch x = 0
-  double* Vh = c.V + c.HW;      // Vh[i*LD + e], e in [-3r, nc + 3r)
   const bool left_b = c.warp == 0, right_b = c.warp == c.NW - 1;
   auto writes_v = [&](int e) {
     return (e >= c.seg && e < c.seg + S) || (left_b && e < 0) || (right_b && e >= c.nc);
@@ -277,7 +328,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       c.zx[xx] = c1_A<R>(w2, c.vx, xx);
     }
     __syncwarp();
-    c1_dots(c, -1);  // lane 0: b.b, lane 1: b.Ab
+    if constexpr (SEGK >= 4) c1_dots_lanes<SEGK>(c, -1); else c1_dots(c, -1);  // rows: b.b, b.Ab
   }
   CL_TR(8)
   __syncthreads();
@@ -341,7 +392,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
             for (int ii = 0; ii < 4; ++ii) {
               const int i = i0 + ii;
               const double a_b = i < j ? coef[i] : 0.0;
-              const double* Vi = Vh + i * LD + e0;
+              const double* Vi = c1_row<(SEGK >= 4)>(c, i < j ? i : 0) + e0;
 #pragma unroll
               for (int k = 0; k < KX; ++k) {
                 const int xx = lane + 32 * k;
@@ -431,7 +482,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       // ---- vector warps: v_j, u_{j+1} = A v_j - hn v_{j-1} - hj v_j, A u_{j+1}, dots
       double* Un = c.U + (pu ^ 1) * LD + c.HW;
       const double inv = coef[CAP];
-      double* Vj = Vh + j * LD;
+      double* Vj = c1_row<(SEGK >= 4)>(c, j);
 #pragma unroll
       for (int k = 0; k < KX; ++k) {
         const int xx = lane + 32 * k;
@@ -446,7 +497,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       double u[KX];
       {
         const double hj = coef[CAP + 1], hb = coef[CAP + 2];
-        const double* Vp = Vh + (j > 0 ? j - 1 : 0) * LD + e0;
+        const double* Vp = c1_row<(SEGK >= 4)>(c, j > 0 ? j - 1 : 0) + e0;
 #pragma unroll
         for (int k = 0; k < KX; ++k) {
           const int xx = lane + 32 * k;
@@ -486,7 +537,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
         c.zx[xx] = c1_A<R>(w2, c.vx, xx);
       }
       __syncwarp();
-      c1_dots(c, j);
+      if constexpr (SEGK >= 4) c1_dots_lanes<SEGK>(c, j); else c1_dots(c, j);
       CL_TR(4)
     }
     __syncthreads();
@@ -529,7 +580,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
     for (int i = 0; i < depth; ++i) {
       const double yi = c.ybuf[i];
 #pragma unroll
-      for (int k = 0; k < SEGK; ++k) x[k] = fma(yi, Vh[i * LD + c.seg + lane + 32 * k], x[k]);
+      for (int k = 0; k < SEGK; ++k) x[k] = fma(yi, c1_row<(SEGK >= 4)>(c, i)[c.seg + lane + 32 * k], x[k]);
     }
   }
   CL_TR(7)
@@ -593,6 +644,7 @@ __global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
     P.ntap = gp->ntap;
     P.cap = gp->cap;
     P.tol = gp->tol;
+    P.K = L.ws ? (int)L.ws_slot : CAP;  // ws_slot carries the resident row count
     for (int k = 0; k < gp->ntap && k < C1_MAXSL; ++k) {
       P.tap_off[k] = gp->tap_off[k];
       P.tap_w[k] = gp->tap_w[k];
@@ -600,7 +652,7 @@ __global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
     for (int d = 0; d <= 2 * P.r; ++d) P.w2[d] = gp->win2_w[d];
   }
   __syncthreads();
-  const C1Layout LY(P.nc, NW, P.S, P.r, C, CAP);
+  const C1Layout LY(P.nc, NW, P.S, P.r, C, CAP, P.K);
   double* sm = reinterpret_cast<double*>(smem_raw + sizeof(C1Params));
   C1Ctx c;
   c.p = &P;
@@ -620,6 +672,8 @@ __global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
   c.q = 0;
   c.vec = c.warp < NW;
   c.V = sm + LY.V;
+  c.K = P.K;
+  c.Vg = L.ws ? L.ws + (size_t)blockIdx.x * (size_t)(CAP - P.K) * P.LD : nullptr;
   c.U = sm + LY.U;
   c.in_row = sm + LY.in_row;
   const int XS = P.S + 6 * P.r + 2;

@@ -336,6 +336,8 @@ struct ClusterVariant {
   int C = 0, P = 0, T = 0, smem = 0, max_clusters = 0;
   bool one_red = false;  // relax_cl1_kernel (one reduction per Arnoldi step)
   int occ = 1;           // CTAs per SM the variant is compiled for
+  int K = 0;             // basis rows resident in shared memory (one_red)
+  double* ws = nullptr;  // per-CTA overflow rows (K < cap)
   const void* fn = nullptr;
 };
 
@@ -399,40 +401,52 @@ void prepare_clusters1(mgb_step* st) {
   for (int d = 0; d <= 2 * r; ++d) wmax = std::max(wmax, std::fabs(hp.win2_w[d]));
   for (int d = 0; d < r; ++d)  // A symmetric (DCGS2 uses u.A V a = a.V^T A u)
     if (std::fabs(hp.win2_w[d] - hp.win2_w[2 * r - d]) > 1e-12 * wmax) return;
-  for (int C : {16, 8, 4, 2}) {
+  for (int C : {16, 8, 4, 2, 1}) {
     if (n % C) continue;
     const int nc = n / C;
     int segk = 0, NW = 0, nwmax = 0;
-    for (int sk : {1, 2}) {
-      if (nc % (32 * sk)) continue;
-      const int nw = nc / (32 * sk);
-      if (nw >= 1 && nw <= 8) { segk = sk; NW = nw; nwmax = 8; break; }
-      if (sk == 2 && nw <= mgb::C1_MAXNW) { segk = sk; NW = nw; nwmax = 16; break; }
+    const int cand[6][2] = {{1, 8}, {2, 8}, {2, 16}, {4, 16}, {8, 8}, {8, 16}};
+    for (const auto& cd : cand) {
+      if (nc % (32 * cd[0])) continue;
+      const int nw = nc / (32 * cd[0]);
+      if (nw >= 1 && nw <= cd[1] && (cd[1] == 8 || nw > 8)) { segk = cd[0]; NW = nw; nwmax = cd[1]; break; }
     }
     if (!segk || 3 * r > nc) continue;
     for (int occ2 = 0; occ2 < 2; ++occ2) {
-    if (occ2 && !(nwmax == 8 && segk == 2 && capt == 20 && r >= 2)) continue;
-    const void* fn = nullptr;
-    {
-      std::lock_guard<std::mutex> lk(reg_mutex());
-      auto it = registry().find(std::make_tuple((int)mgb::K_SLGC1, segk, capt, r, occ2 ? 108 : nwmax));
-      if (it == registry().end()) continue;
-      fn = it->second;
-    }
-    ClusterVariant v;
-    v.C = C;
-    v.P = segk;
-    v.T = 32 * (NW + 1);
-    v.fn = fn;
-    v.one_red = true;
-    v.occ = occ2 ? 2 : 1;
-    v.smem = (int)mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt);
-    if (v.smem > 227 * 1024) continue;
-    const bool ok = try_cluster_variant(v);
-    if (std::getenv("MGB_DEBUG"))
-      fprintf(stderr, "[mgb] cl1 variant n=%d C=%d segk=%d T=%d occ2=%d smem=%d ok=%d max_clusters=%d\n", n, C,
-              segk, v.T, occ2, v.smem, (int)ok, v.max_clusters);
-    if (ok) st->clusters1.push_back(v);
+      if (occ2 && !(nwmax == 8 && segk == 2 && capt == 20 && r >= 2)) continue;
+      const void* fn = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(reg_mutex());
+        auto it = registry().find(std::make_tuple((int)mgb::K_SLGC1, segk, capt, r, occ2 ? 108 : nwmax));
+        if (it == registry().end()) continue;
+        fn = it->second;
+      }
+      ClusterVariant v;
+      v.C = C;
+      v.P = segk;
+      v.T = 32 * (NW + 1);
+      v.fn = fn;
+      v.one_red = true;
+      v.occ = occ2 ? 2 : 1;
+      const size_t budget = occ2 ? 113 * 1024 : 227 * 1024;
+      int K = capt;
+      while (K > 1 && mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt, K) > budget) --K;
+      v.K = K;
+      v.smem = (int)mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt, K);
+      if ((size_t)v.smem > budget) continue;
+      const bool ok = try_cluster_variant(v);
+      if (std::getenv("MGB_DEBUG"))
+        fprintf(stderr, "[mgb] cl1 variant n=%d C=%d segk=%d T=%d occ2=%d K=%d smem=%d ok=%d max_clusters=%d\n", n,
+                C, segk, v.T, occ2, K, v.smem, (int)ok, v.max_clusters);
+      if (!ok) continue;
+      if (K < capt) {  // overflow rows: one slot of (cap - K) halo'd rows per resident CTA
+        const size_t rows = (size_t)(capt - K) * mgb::c1_ld(nc, r);
+        if (cudaMalloc(&v.ws, rows * 8 * (size_t)v.max_clusters * C) != cudaSuccess) {
+          cudaGetLastError();
+          continue;
+        }
+      }
+      st->clusters1.push_back(v);
     }
   }
 }
@@ -662,6 +676,8 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
 
 void mgb_step_destroy(mgb_step* st) {
   if (!st) return;
+  for (ClusterVariant& v : st->clusters1)
+    if (v.ws) cudaFree(v.ws);
   if (st->dp) cudaFree(st->dp);
   if (st->ws) cudaFree(st->ws);
   delete st;
@@ -718,11 +734,15 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
       if (force_c && v.C != force_c) continue;
       static const bool no_occ2 = std::getenv("MGB_C1_NO_OCC2") != nullptr;
       if (no_occ2 && v.occ == 2) continue;
+      // wide segments (cluster sizes 1-2 on 4096-point rows) measured slower than
+      // the single-CTA kernel for many-interval levels: opt-in only
+      static const bool wide = std::getenv("MGB_C1_WIDE") != nullptr;
+      if (v.P >= 4 && !wide && !force_c) continue;
       const long long w = (a->n_intervals + v.max_clusters - 1) / v.max_clusters;
       if (!best || w < best_w) { best = &v; best_w = w; }
     }
     static const long long max_waves1 = std::getenv("MGB_C1_WAVES")
-                                            ? std::atoll(std::getenv("MGB_C1_WAVES")) : 2;
+                                            ? std::atoll(std::getenv("MGB_C1_WAVES")) : (1LL << 40);
     if (best && best_w <= max_waves1) {
       const ClusterVariant& v = *best;
       const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
@@ -739,7 +759,10 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
       const StepParams* dpc = st->dp;
-      void* cargs[] = {(void*)&dpc, (void*)&L};
+      mgb::RelaxLaunch L1 = L;
+      L1.ws = v.ws;         // overflow basis rows (nullptr: all resident)
+      L1.ws_slot = v.K;     // resident row count
+      void* cargs[] = {(void*)&dpc, (void*)&L1};
       CUDA_TRY(cudaLaunchKernelExC(&cfg, v.fn, cargs));
       g_launches++;
       return MGB_OK;
