@@ -741,8 +741,9 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
       const long long w = (a->n_intervals + v.max_clusters - 1) / v.max_clusters;
       if (!best || w < best_w) { best = &v; best_w = w; }
     }
+    // many-interval levels (> 2 cluster waves) run faster on the single-CTA kernel
     static const long long max_waves1 = std::getenv("MGB_C1_WAVES")
-                                            ? std::atoll(std::getenv("MGB_C1_WAVES")) : (1LL << 40);
+                                            ? std::atoll(std::getenv("MGB_C1_WAVES")) : 2;
     if (best && best_w <= max_waves1) {
       const ClusterVariant& v = *best;
       const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
