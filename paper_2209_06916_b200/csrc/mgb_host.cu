@@ -406,7 +406,9 @@ void prepare_clusters1(mgb_step* st) {
     const int nc = n / C;
     int segk = 0, NW = 0, nwmax = 0;
     const int cand[6][2] = {{1, 8}, {2, 8}, {2, 16}, {4, 16}, {8, 8}, {8, 16}};
+    static const int min_segk = std::getenv("MGB_C1_SEGK") ? std::atoi(std::getenv("MGB_C1_SEGK")) : 1;
     for (const auto& cd : cand) {
+      if (cd[0] < min_segk) continue;
       if (nc % (32 * cd[0])) continue;
       const int nw = nc / (32 * cd[0]);
       if (nw >= 1 && nw <= cd[1] && (cd[1] == 8 || nw > 8)) { segk = cd[0]; NW = nw; nwmax = cd[1]; break; }
