@@ -19,6 +19,8 @@ void register_gen() {
   GEN_P(4)
   GEN_P(8)
   GEN_P(16)
+  MGB_REG(K_GEN, 32, 0, 1, true);
+  MGB_REG(K_GEN, 32, 0, 1, false);
 }
 }  // namespace mgb
 

@@ -19,6 +19,10 @@ namespace mgb {
   MGB_REG(K_WIN, P, 16, 2, true);  \
   MGB_REG(K_WIN, P, 30, 2, true);
 void register_win_exact() {
+  // n_x = 16384 (cfg5): 32 points per thread, 512 threads, generic single-buffer slice
+  MGB_REG(K_WIN, 32, 1, 2, true);
+  MGB_REG(K_WIN, 32, 9, 2, true);
+  MGB_REG(K_WIN, 32, 30, 2, true);
   WIN_P(4)
   WIN_P(8)
   WIN_P(16)

@@ -18,6 +18,9 @@ namespace mgb {
   MGB_REG(K_WIN, P, 16, 2, false);  \
   MGB_REG(K_WIN, P, 30, 2, false);
 void register_win_fast() {
+  MGB_REG(K_WIN, 32, 1, 2, false);
+  MGB_REG(K_WIN, 32, 9, 2, false);
+  MGB_REG(K_WIN, 32, 30, 2, false);
   WIN_P(4)
   WIN_P(8)
   WIN_P(16)

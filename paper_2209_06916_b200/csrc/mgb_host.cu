@@ -292,11 +292,11 @@ int choose_layout(int kind, int n, int& P, int& T, int& S) {
       break;
     }
   }
-  while (n / P > 512 && P < 16 && n % (2 * P) == 0) P *= 2;
+  while (n / P > 512 && P < 32 && n % (2 * P) == 0) P *= 2;
   T = n / P;
   if (T > 512 || T * P != n)
     return fail(MGB_ERR_UNSUPPORTED, "n_x=" + std::to_string(n) +
-                                         " outside the single-CTA slice envelope (need n_x = T*P, T<=512, P<=16)");
+                                         " outside the single-CTA slice envelope (need n_x = T*P, T<=512, P<=32)");
   const int want = (P >= 16) ? 1 : 16 / P;
   S = T;
   while (S % 16 != want % 16) ++S;
@@ -591,6 +591,10 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     }
   }
   hp.gain_inv = 1.0;
+  if (((dk == mgb::K_RK && hp.implicit) || dk == mgb::K_SLD) && P > mgb::MAXP) {
+    delete st;
+    return fail(MGB_ERR_UNSUPPORTED, "implicit banded solves support n_x <= " + std::to_string(512 * mgb::MAXP));
+  }
   if ((dk == mgb::K_RK && hp.implicit) || dk == mgb::K_SLD) {
     if (d->n_taps2 < 1) { delete st; return fail(MGB_ERR_INVALID, "implicit operator stencil missing"); }
     std::vector<long long> o2(d->offsets2, d->offsets2 + d->n_taps2);
@@ -644,6 +648,24 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->smem = (int)(sizeof(StepParams) + 8 * dbl);
   if (win_dedicated)  // relax_win_kernel: double-buffered slice, weights in registers
     st->smem = (int)(8 * (2 * (size_t)P * S + 32));  // 2 slices + reduction
+  // SL + GMRES on rows whose single-CTA slice + TMA stages exceed shared memory
+  // (n_x > 8192): cluster kernels only
+  const bool cluster_only = dk == mgb::K_SLG && st->smem > 227 * 1024;
+  if (cluster_only) {
+    st->fn = nullptr;
+    st->max_grid = 0;
+    prepare_clusters(st);
+    if (st->clusters1.empty()) {
+      delete st;
+      return fail(MGB_ERR_UNSUPPORTED, "no cluster GMRES variant for n_x=" + std::to_string(n));
+    }
+    cudaError_t e0 = cudaMalloc(&st->dp, sizeof(StepParams));
+    if (e0 != cudaSuccess) { delete st; return fail(MGB_ERR_CUDA, "cudaMalloc params"); }
+    e0 = cudaMemcpy(st->dp, &hp, sizeof(StepParams), cudaMemcpyHostToDevice);
+    if (e0 != cudaSuccess) { cudaFree(st->dp); delete st; return fail(MGB_ERR_CUDA, "upload params"); }
+    *out = st;
+    return MGB_OK;
+  }
   {
     std::lock_guard<std::mutex> lk(reg_mutex());
     auto it = registry().end();
@@ -696,7 +718,7 @@ int mgb_step_layout(const mgb_step* st, int32_t* threads, int32_t* ppt, int32_t*
 int mgb_step_reserve_workspace(mgb_step* st, void* stream) {
   (void)stream;
   if (!st) return fail(MGB_ERR_INVALID, "null step");
-  if (st->dkind != mgb::K_SLG || st->ws) return MGB_OK;
+  if (st->dkind != mgb::K_SLG || st->ws || !st->fn) return MGB_OK;
   const long long cap = st->hp.cap, n = st->hp.n;
   st->ws_slot = (cap + 1) * n + cap * cap + 3 * cap + 1;
   st->ws_slot = (st->ws_slot + 31) / 32 * 32;
@@ -746,7 +768,7 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
     // many-interval levels (> 2 cluster waves) run faster on the single-CTA kernel
     static const long long max_waves1 = std::getenv("MGB_C1_WAVES")
                                             ? std::atoll(std::getenv("MGB_C1_WAVES")) : 2;
-    if (best && best_w <= max_waves1) {
+    if (best && (best_w <= max_waves1 || !st->fn)) {
       const ClusterVariant& v = *best;
       const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
       cudaLaunchConfig_t cfg = {};
@@ -796,6 +818,7 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
       return MGB_OK;
     }
   }
+  if (!st->fn) return fail(MGB_ERR_UNSUPPORTED, "this plan runs on cluster kernels only (n_x too long for one CTA)");
   if (st->dkind == mgb::K_SLG) {
     int rc = mgb_step_reserve_workspace(st, stream);
     if (rc) return rc;

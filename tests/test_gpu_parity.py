@@ -55,7 +55,8 @@ def test_shift_and_identity(n):
 # ------------------------------------------------------------- f-relaxation
 
 @pytest.mark.parametrize("p,c,n,nt,m", [(1, 0.85, 1024, 1024, 8), (3, 0.85, 4096, 256, 8),
-                                        (5, 0.85, 512, 256, 16), (3, 1.382, 64, 64, 4)])
+                                        (5, 0.85, 512, 256, 16), (3, 1.382, 64, 64, 4),
+                                        (3, 0.85, 16384, 64, 8)])
 def test_f_relax_bitwise(p, c, n, nt, m):
     spec = P.DiscretizationSpec("erk", p, c, n, nt)
     st = P.mol_stepper(spec)
@@ -213,7 +214,8 @@ def oracle_envelope(fam, p, c, n_x, n_t, m, cycle):
 
 
 @pytest.mark.parametrize("p,cf,m,n_x,n_t", [(3, 0.85, 8, 256, 1024), (1, 0.85, 4, 256, 1024),
-                                            (3, None, 8, 256, 1024), (5, None, 16, 256, 4096)])
+                                            (3, None, 8, 256, 1024), (5, None, 16, 256, 4096),
+                                            (3, None, 8, 16384, 512)])
 def test_erk_vcycle_gmres_history(p, cf, m, n_x, n_t):
     """GMRES-corrected V-cycles: identical iteration count; history and final
     iterate within 10x the oracle's self-noise envelope (floors 1e-13 / 1e-12)."""
