@@ -586,7 +586,7 @@ def build_hierarchy(family, p, c, n_x, n_t, m, cycle, kind="modified", q=None,
                 break
             factors.append(mf)
             rem //= mf
-    solver = "gmres" if (family == "erk" and cycle == "v_cycle" and kind == "modified") \
+    solver = "gmres" if (family == "erk" and cycle in ("v_cycle", "f_cycle") and kind == "modified") \
         else "direct"
     steps, cum = [fine], 1
     for level, mf in enumerate(factors, start=1):
@@ -702,7 +702,12 @@ class Mgrit:
         g[0] = self.u0
         return g
 
-    def cycle_once(self, level, u, g):
+    def cycle_once(self, level, u, g, kind=None):
+        """One cycle on ``level`` (mgrit.py:225-247).  ``kind="f_cycle"`` is the
+        builder's extension (no reference counterpart, parity unpinned by the
+        reference): the coarse problem is solved by an F-cycle from e = 0
+        followed by one V-cycle from that result."""
+        kind = kind or self.cycle
         step, m = self.steps[level], self.factors[level]
         pool, thr = self.pool, self.threads
         f_relax(u, g, step, m, pool, thr)
@@ -711,11 +716,15 @@ class Mgrit:
             f_relax(u, g, step, m, pool, thr)
         r = restrict(u, g, step, m, pool, thr)
         gc = np.vstack([np.zeros((1, len(self.u0))), r])
-        if self.cycle == "two_level" or level + 1 == len(self.factors):
+        if kind == "two_level" or level + 1 == len(self.factors):
             e = forward_substitute(self.steps[level + 1], gc)
+        elif kind == "f_cycle":
+            e = np.zeros_like(gc)
+            self.cycle_once(level + 1, e, gc, "f_cycle")
+            self.cycle_once(level + 1, e, gc, "v_cycle")
         else:
             e = np.zeros_like(gc)
-            self.cycle_once(level + 1, e, gc)
+            self.cycle_once(level + 1, e, gc, "v_cycle")
         u[m::m] += e[1:]
         f_relax(u, g, step, m, pool, thr)
 

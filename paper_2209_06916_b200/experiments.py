@@ -63,6 +63,7 @@ def level_factors(n_t: int, m, cycle: str, coarse_kind: str) -> List[int]:
     m_list = [m] if np.isscalar(m) else list(m)
     if cycle == "two_level" or coarse_kind in ("ideal", "rediscretized"):
         return m_list[:1]
+    # v_cycle and (extension) f_cycle share the multilevel hierarchy
     factors: List[int] = []
     n = n_t
     while True:
@@ -84,7 +85,7 @@ def build_problem(spec: DiscretizationSpec, m, cycle: str, coarse_kind: str = "m
     """
     fine = fine_stepper(spec, tab)
     factors = level_factors(spec.n_t, m, cycle, coarse_kind)
-    solver = "gmres" if (spec.family == "erk" and cycle == "v_cycle"
+    solver = "gmres" if (spec.family == "erk" and cycle in ("v_cycle", "f_cycle")
                          and coarse_kind == "modified") else "direct"
     steppers = [fine]
     cumulative = 1

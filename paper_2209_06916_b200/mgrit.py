@@ -49,7 +49,9 @@ class MgritConfig:
     def __post_init__(self):
         if self.nu < 0:
             raise ValueError(f"nu must be >= 0, got {self.nu}")
-        if self.cycle not in ("two_level", "v_cycle"):
+        # "f_cycle" is an extension (the reference has two_level | v_cycle,
+        # mgrit.py:41-42; BASELINE cfg5 names an F-cycle)
+        if self.cycle not in ("two_level", "v_cycle", "f_cycle"):
             raise ValueError(f"unknown cycle {self.cycle!r}")
         if self.max_iters < 1:
             raise ValueError("max_iters must be >= 1")
@@ -298,8 +300,10 @@ class MgritSolver:
             out[name] = (cnt + 1, ms + s.elapsed_time(e))
         return out
 
-    def _cycle(self, l: int, u: int, g: Optional[int], u_zero: bool, want_norm: bool) -> None:
+    def _cycle(self, l: int, u: int, g: Optional[int], u_zero: bool, want_norm: bool,
+               kind: Optional[str] = None) -> None:
         cfg = self.config
+        kind = kind or cfg.cycle
         L = self.levels[l]
         n = self.problem.n_x
         m, nI, plan = L.m, L.n_int, L.plan
@@ -321,7 +325,7 @@ class MgritSolver:
         self._timed(f"L{l}.FR", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
                     c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
                     tail_out=ptr(gC) + row, tail_stride=n, g=g)
-        self._coarse_solve(l + 1)
+        self._coarse_solve(l + 1, kind)
         fuse_norm = want_norm and cfg.nu > 0
         if cfg.nu == 0:
             c_src, c_stride = (None if u_zero else u), m * n
@@ -337,16 +341,23 @@ class MgritSolver:
         if want_norm and not fuse_norm:
             self._timed("L0.R", self._residual_partials, u, g)
 
-    def _coarse_solve(self, child: int) -> None:
+    def _coarse_solve(self, child: int, kind: Optional[str] = None) -> None:
         """Solve level ``child`` for e = ucoarse[child] given g = gcoarse[child]:
         forward substitution (two-level / coarsest) or a recursive cycle from
-        e = 0 (mgrit.py:239-244)."""
+        e = 0 (mgrit.py:239-244).  F-cycle (extension): an F-cycle on the child
+        from e = 0 followed by one V-cycle on the child from that result (the
+        multigrid F-cycle: the W-cycle with its second recursive call replaced
+        by a V-cycle); on two-level hierarchies it equals the V-cycle."""
+        kind = kind or self.config.cycle
         uC, gC = self.ucoarse[child], self.gcoarse[child]
-        if self.config.cycle == "two_level" or child == len(self.levels):
+        if kind == "two_level" or child == len(self.levels):
             self._timed(f"L{child}.seq", _forward_substitute_dev, self.plans[child], ptr(uC),
                         ptr(gC), self.problem.points_on_level(child))
+        elif kind == "f_cycle":
+            self._cycle(child, ptr(uC), ptr(gC), True, False, "f_cycle")
+            self._cycle(child, ptr(uC), ptr(gC), False, False, "v_cycle")
         else:
-            self._cycle(child, ptr(uC), ptr(gC), True, False)
+            self._cycle(child, ptr(uC), ptr(gC), True, False, "v_cycle")
 
     def _residual_partials(self, u: int, g: Optional[int]) -> None:
         L = self.levels[0]
