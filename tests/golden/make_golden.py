@@ -189,11 +189,31 @@ def history_fixture(full: bool):
         print(name, rep.iterations, f"{wall:.1f}s", flush=True)
 
 
+def cli_fixture():
+    """Reference CLI output (cli.py solve/iters) for the CLI parity tests."""
+    from mgrit_advection import cli as RCLI
+    runs = {
+        "cli_solve_erk1_tl.csv": ["solve", "--family", "erk", "--p", "1", "--c", "0.85", "--grid",
+                                  "64,256", "--m", "4", "--cycle", "two-level", "--threads", "1"],
+        "cli_solve_sdirk3_v.csv": ["solve", "--family", "sdirk", "--p", "3", "--c", "4", "--grid",
+                                   "64,256", "--m", "4", "--cycle", "v", "--threads", "1"],
+        "cli_iters_erk3.csv": ["iters", "--family", "erk", "--p", "3", "--c-fraction", "0.85",
+                               "--grid", "64,256", "--m", "4,8", "--threads", "1"],
+    }
+    for name, argv in runs.items():
+        path = os.path.join(HERE, name)
+        assert RCLI.main(argv + ["--out", path]) == 0
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--only-full", action="store_true")
+    ap.add_argument("--cli", action="store_true")
     a = ap.parse_args()
+    if a.cli:
+        cli_fixture()
+        raise SystemExit(0)
     if not a.only_full:
         setup_fixture()
         relax_fixture()
