@@ -52,8 +52,16 @@ struct C1Params {
 };
 static_assert(sizeof(C1Params) % 16 == 0, "C1Params must be 16-byte sized");
 
-// odd row stride: the transposed dot products (lane i reads row i) are bank-conflict free
-__host__ __device__ inline int c1_ld(int nc, int r) { return nc + 6 * r + 1; }
+// row stride = 2 (mod 4) doubles: the transposed dot products (lane i reads row i
+// with 16-byte loads) are bank-conflict free
+__host__ __device__ inline int c1_ld(int nc, int r) {
+  int ld = nc + 6 * r + 1;
+  while (ld % 4 != 2) ++ld;
+  return ld;
+}
+// scratch row of a warp: the extended segment + a one-double shift so that the
+// own points (offset 3r) start 16-byte aligned
+__host__ __device__ inline int c1_xs(int S, int r) { return (S + 6 * r + 4) & ~1; }
 
 // shared-memory layout (doubles, after the C1Params block).  The step input row
 // of the SL stencil aliases U[1]'s own points: it is read by peers only before
@@ -62,12 +70,14 @@ struct C1Layout {
   int V, U, in_row, scr, cred, wred, Hm, R, cs, sn, gg, ybuf, hc, flg, total;
   __host__ __device__ C1Layout(int nc, int NW, int S, int r, int C, int CAP, int K) {
     const int LD = c1_ld(nc, r);
-    const int XS = S + 6 * r + 2;
+    const int XS = c1_xs(S, r);
     int o = 0;
-    V = o;      o += (K < CAP ? K : CAP) * LD;
+    V = o;      o += (K < CAP ? K : CAP) * LD + 2;  // + shift: rows' own points 16-byte aligned
     U = o;      o += 2 * LD;
     in_row = U + LD + 3 * r;
-    scr = o;    o += NW * 2 * XS;
+    o = (o + 1) & ~1;
+    scr = o;    o += NW * 2 * XS + 2;
+    o = (o + 1) & ~1;
     cred = o;   o += 2 * C * C1_SLOTS;
     wred = o;   o += NW * C1_SLOTS;
     Hm = o;  // (unused)
@@ -213,18 +223,22 @@ __device__ __forceinline__ double c1_sl(const C1Ctx& c, cg::cluster_group& cl, i
 
 // Transposed partial dots of this warp's segment for reduction R_{j+1}: lane
 // i <= j: V_i.u, lane j+1: u.u, lane j+2: u.Au (u = vx[3r..], Au = zx[3r..]).
-// No shuffles; rows are read with an odd stride (conflict-free), u broadcast.
+// No shuffles; 16-byte loads of rows whose stride is 2 (mod 4) doubles
+// (conflict-free), u broadcast.
 __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
   const int lane = c.lane, S = c.S, off = 3 * c.r;
   if (lane <= j + 2) {
     const double* uu = c.vx + off;
     const double* vr = lane <= j ? c1_row<false>(c, lane) + c.seg : (lane == j + 1 ? uu : c.zx + off);
+    const double2* v2 = reinterpret_cast<const double2*>(vr);
+    const double2* u2 = reinterpret_cast<const double2*>(uu);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int e = 0; e < S; e += 4) {
-      a0 = fma(vr[e], uu[e], a0);
-      a1 = fma(vr[e + 1], uu[e + 1], a1);
-      a2 = fma(vr[e + 2], uu[e + 2], a2);
-      a3 = fma(vr[e + 3], uu[e + 3], a3);
+    for (int e = 0; e < S / 2; e += 2) {
+      const double2 x0 = v2[e], x1 = v2[e + 1], y0 = u2[e], y1 = u2[e + 1];
+      a0 = fma(x0.x, y0.x, a0);
+      a1 = fma(x0.y, y0.y, a1);
+      a2 = fma(x1.x, y1.x, a2);
+      a3 = fma(x1.y, y1.y, a3);
     }
     c.wred[c.warp * C1_SLOTS + lane] = (a0 + a1) + (a2 + a3);
   }
@@ -671,13 +685,13 @@ __global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
   c.base = c.rank * P.nc;
   c.q = 0;
   c.vec = c.warp < NW;
-  c.V = sm + LY.V;
+  c.V = sm + LY.V + (P.HW & 1);  // c.V + HW (own point 0 of row 0) is 16-byte aligned
   c.K = P.K;
   c.Vg = L.ws ? L.ws + (size_t)blockIdx.x * (size_t)(CAP - P.K) * P.LD : nullptr;
   c.U = sm + LY.U;
   c.in_row = sm + LY.in_row;
-  const int XS = P.S + 6 * P.r + 2;
-  c.vx = sm + LY.scr + (c.vec ? c.warp : 0) * 2 * XS;
+  const int XS = c1_xs(P.S, P.r);
+  c.vx = sm + LY.scr + (c.vec ? c.warp : 0) * 2 * XS + ((3 * P.r) & 1);
   c.zx = c.vx + XS;
   c.cred = sm + LY.cred;
   c.wred = sm + LY.wred;

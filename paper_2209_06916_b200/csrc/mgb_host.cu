@@ -46,6 +46,20 @@ std::map<std::tuple<int, int, int, int, int>, const void*>& registry() {
   static std::map<std::tuple<int, int, int, int, int>, const void*> r;
   return r;
 }
+// The max-dynamic-shared-memory attribute belongs to the kernel FUNCTION, which
+// several plans (different n_x) share: only ever raise it, so a later smaller
+// plan cannot invalidate the launches of an earlier larger one.
+cudaError_t raise_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<const void*, int> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = cur[fn];
+  if (bytes <= have) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 void ensure_registered() {
   static std::once_flag once;
   std::call_once(once, [] {
@@ -359,7 +373,7 @@ namespace {
 // Cluster launch variants for SL_GMRES: C CTAs per interval, P <= 2 points per
 // thread, 32 <= T <= 256 threads per CTA, column cap 10 or 20.
 bool try_cluster_variant(ClusterVariant& v) {
-  if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem) != cudaSuccess) {
+  if (raise_smem_attr(v.fn, v.smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -491,7 +505,7 @@ void prepare_clusters(mgb_step* st) {
     v.fn = fn;
     v.smem = (int)(sizeof(StepParams) + 8 * (size_t)(capt == 10 ? mgb::ClLayout<10>::total(nc)
                                                                   : mgb::ClLayout<20>::total(nc)));
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem) != cudaSuccess) continue;
+    if (raise_smem_attr(fn, v.smem) != cudaSuccess) continue;
     if (C > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
       cudaGetLastError();
       continue;
@@ -677,7 +691,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     if (it == registry().end()) { delete st; return fail(MGB_ERR_UNSUPPORTED, "no kernel instantiation for this layout"); }
     st->fn = it->second;
   }
-  cudaError_t e = cudaFuncSetAttribute(st->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, st->smem);
+  cudaError_t e = raise_smem_attr(st->fn, st->smem);
   if (e != cudaSuccess) { delete st; return fail(MGB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)); }
   int nb = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
