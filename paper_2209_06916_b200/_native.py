@@ -13,7 +13,9 @@ from typing import Optional
 
 from .errors import DimensionMismatchError, SingularOperatorError
 
-_LIB_NAME = "libmgrit_b200_trace.so" if os.environ.get("MGB_TRACE") else "libmgrit_b200.so"
+# MGB_LIB selects an experimental build of the same library (tools/build_variant.sh)
+_LIB_NAME = os.environ.get("MGB_LIB") or (
+    "libmgrit_b200_trace.so" if os.environ.get("MGB_TRACE") else "libmgrit_b200.so")
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", _LIB_NAME)
 
 MGB_OK, MGB_ERR_INVALID, MGB_ERR_DIMENSION, MGB_ERR_SINGULAR, MGB_ERR_CUDA, MGB_ERR_UNSUPPORTED = range(6)

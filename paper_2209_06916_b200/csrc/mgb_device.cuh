@@ -1123,6 +1123,10 @@ __device__ __forceinline__ void slice_to_global(const double* row, double* dst, 
 #ifndef MGB_WIN_MINB
 #define MGB_WIN_MINB 2
 #endif
+#ifndef MGB_WIN_U
+#define MGB_WIN_U 4
+#endif
+constexpr int WIN_U = MGB_WIN_U;  // row loads in flight per thread at interval head / tail
 // one thread issues an L2 prefetch of a contiguous byte range (no registers, no completion)
 __device__ __forceinline__ void l2_prefetch(const void* g, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
@@ -1157,16 +1161,28 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
     const double* erow = (a.e && kg >= 1) ? a.e + k * a.e_stride : nullptr;
     __syncthreads();  // previous interval's readers of both buffers are done
     // interval start: C-point (+ correction, mgrit.py:246) -> slice buffer 0 (and c_out)
-    for (int i = 2 * t; i < n; i += 2 * nthr) {
-      double2 y = csrc ? __ldg(reinterpret_cast<const double2*>(csrc + i)) : make_double2(0.0, 0.0);
-      if (erow) {
-        const double2 ev = __ldg(reinterpret_cast<const double2*>(erow + i));
-        y.x = __dadd_rn(y.x, ev.x);
-        y.y = __dadd_rn(y.y, ev.y);
+    // loads batched WIN_U deep (all in flight before the first use)
+    for (int i0 = 2 * t; i0 < n; i0 += 2 * nthr * WIN_U) {
+      double2 y[WIN_U], ev[WIN_U];
+#pragma unroll
+      for (int u = 0; u < WIN_U; ++u) {
+        const int i = i0 + 2 * nthr * u;
+        y[u] = (csrc && i < n) ? __ldg(reinterpret_cast<const double2*>(csrc + i)) : make_double2(0.0, 0.0);
+        ev[u] = (erow && i < n) ? __ldg(reinterpret_cast<const double2*>(erow + i)) : make_double2(0.0, 0.0);
       }
-      if (a.c_out) *reinterpret_cast<double2*>(a.c_out + k * a.c_out_stride + i) = y;
-      row0[saddr<P>(i, S)] = y.x;
-      row0[saddr<P>(i + 1, S)] = y.y;
+#pragma unroll
+      for (int u = 0; u < WIN_U; ++u) {
+        const int i = i0 + 2 * nthr * u;
+        if (i < n) {
+          if (erow) {
+            y[u].x = __dadd_rn(y[u].x, ev[u].x);
+            y[u].y = __dadd_rn(y[u].y, ev[u].y);
+          }
+          if (a.c_out) *reinterpret_cast<double2*>(a.c_out + k * a.c_out_stride + i) = y[u];
+          row0[saddr<P>(i, S)] = y[u].x;
+          row0[saddr<P>(i + 1, S)] = y[u].y;
+        }
+      }
     }
     if (t == 0) {  // warm L2 for the next interval this CTA handles
       const long long kn = k + gridDim.x;
@@ -1206,26 +1222,41 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
       __syncthreads();
       const long long grow = rowbase + a.m;
       double part = 0.0;
-      for (int i = 2 * t; i < n; i += 2 * nthr) {
-        double2 z = make_double2(zb[saddr<P>(i, S)], zb[saddr<P>(i + 1, S)]);
-        if (a.g) {
-          const double2 gv = __ldg(reinterpret_cast<const double2*>(a.g + grow * n + i));
-          z.x = __dadd_rn(gv.x, z.x);  // g + Phi u (commutative: bitwise either order)
-          z.y = __dadd_rn(gv.y, z.y);
+      const double* gsrc = a.g ? a.g + grow * n : nullptr;
+      const double* crow = a.tail == 2 ? a.cref + k * a.cref_stride : nullptr;
+      const double* cerow = (a.tail == 2 && a.cref_e) ? a.cref_e + k * a.cref_e_stride : nullptr;
+      for (int i0 = 2 * t; i0 < n; i0 += 2 * nthr * WIN_U) {
+        double2 gv[WIN_U], c[WIN_U], ce[WIN_U];
+#pragma unroll
+        for (int u = 0; u < WIN_U; ++u) {  // loads batched WIN_U deep
+          const int i = i0 + 2 * nthr * u;
+          const bool in = i < n;
+          gv[u] = (gsrc && in) ? __ldg(reinterpret_cast<const double2*>(gsrc + i)) : make_double2(0.0, 0.0);
+          c[u] = (crow && in) ? __ldg(reinterpret_cast<const double2*>(crow + i)) : make_double2(0.0, 0.0);
+          ce[u] = (cerow && in) ? __ldg(reinterpret_cast<const double2*>(cerow + i)) : make_double2(0.0, 0.0);
         }
-        if (a.tail == 1) {  // C-relaxation (mgrit.py:148-149)
-          *reinterpret_cast<double2*>(a.tail_out + k * a.tail_stride + i) = z;
-        } else {  // residual (g + Phi u) - u_C (mgrit.py:159-161)
-          double2 c = __ldg(reinterpret_cast<const double2*>(a.cref + k * a.cref_stride + i));
-          if (a.cref_e) {
-            const double2 ce = __ldg(reinterpret_cast<const double2*>(a.cref_e + k * a.cref_e_stride + i));
-            c.x = __dadd_rn(c.x, ce.x);
-            c.y = __dadd_rn(c.y, ce.y);
+#pragma unroll
+        for (int u = 0; u < WIN_U; ++u) {
+          const int i = i0 + 2 * nthr * u;
+          if (i >= n) continue;
+          double2 z = make_double2(zb[saddr<P>(i, S)], zb[saddr<P>(i + 1, S)]);
+          if (gsrc) {
+            z.x = __dadd_rn(gv[u].x, z.x);  // g + Phi u (commutative: bitwise either order)
+            z.y = __dadd_rn(gv[u].y, z.y);
           }
-          const double2 r = make_double2(__dsub_rn(z.x, c.x), __dsub_rn(z.y, c.y));
-          part = fma(r.x, r.x, part);
-          part = fma(r.y, r.y, part);
-          if (a.tail_out) *reinterpret_cast<double2*>(a.tail_out + k * a.tail_stride + i) = r;
+          if (a.tail == 1) {  // C-relaxation (mgrit.py:148-149)
+            *reinterpret_cast<double2*>(a.tail_out + k * a.tail_stride + i) = z;
+          } else {  // residual (g + Phi u) - u_C (mgrit.py:159-161)
+            double2 cc = c[u];
+            if (cerow) {
+              cc.x = __dadd_rn(cc.x, ce[u].x);
+              cc.y = __dadd_rn(cc.y, ce[u].y);
+            }
+            const double2 r = make_double2(__dsub_rn(z.x, cc.x), __dsub_rn(z.y, cc.y));
+            part = fma(r.x, r.x, part);
+            part = fma(r.y, r.y, part);
+            if (a.tail_out) *reinterpret_cast<double2*>(a.tail_out + k * a.tail_stride + i) = r;
+          }
         }
       }
       if (a.tail == 2 && a.partials) {
