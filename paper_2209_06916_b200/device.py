@@ -198,10 +198,12 @@ def device_sum(partials, n: int, out, stream=None) -> None:
 _PLAN_CACHE: dict = {}
 
 
-def plan_for(prog: DeviceProgram) -> StepPlan:
-    """Memoised device plan per (program, device)."""
+def plan_for(prog: DeviceProgram, tag=None) -> StepPlan:
+    """Memoised device plan per (program, device, tag).  Plans own their GMRES
+    workspaces, so solves that run concurrently on different CUDA streams pass
+    distinct tags (``solve_many`` uses the stream) to get private plans."""
     torch = require_cuda()
-    key = (torch.cuda.current_device(), prog.key())
+    key = (torch.cuda.current_device(), tag, prog.key())
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         plan = StepPlan(prog)

@@ -124,19 +124,45 @@ class IterationCell:
 def iteration_table(family: str, p: int, c: float, grids: Sequence[tuple],
                     m_values: Sequence[int], coarse_kind: str = "modified", nu: int = 1,
                     max_iters: int = 40, rng_seed: int = 0,
-                    threads: int = 1) -> List[IterationCell]:
-    """Two-level and V-cycle iteration counts (experiments.py:221-242), on the GPU."""
-    cells = []
+                    threads: int = 1, concurrent: bool = False) -> List[IterationCell]:
+    """Two-level and V-cycle iteration counts (experiments.py:221-242), on the GPU.
+
+    ``concurrent=True`` (extension) runs every cell's solves at once through
+    ``mgrit.solve_many`` (one CUDA stream per solve); the reports are bitwise
+    identical to the sequential ones."""
+    keys, jobs = [], []
     for n_x, n_t in grids:
         for m in m_values:
             spec = DiscretizationSpec(family, p, c, n_x, n_t)
-            reps = {}
             for cycle in ("two_level", "v_cycle"):
                 cfg = mgrit.MgritConfig(nu=nu, cycle=cycle, tol=1e-10, max_iters=max_iters,
                                         rng_seed=rng_seed)
-                reps[cycle] = mgrit.solve(build_problem(spec, m, cycle, coarse_kind), cfg,
-                                          threads=threads)
-            fmt = lambda r: str(r.iterations) if r.converged else f">{max_iters}"
-            cells.append(IterationCell(n_x, n_t, m, fmt(reps["two_level"]), fmt(reps["v_cycle"]),
-                                       reps["two_level"], reps["v_cycle"]))
+                keys.append((n_x, n_t, m, cycle))
+                jobs.append((build_problem(spec, m, cycle, coarse_kind), cfg))
+    if concurrent:
+        reports = mgrit.solve_many(jobs)
+    else:
+        reports = [mgrit.solve(pr, cfg, threads=threads) for pr, cfg in jobs]
+    by = dict(zip(keys, reports))
+    fmt = lambda r: str(r.iterations) if r.converged else f">{max_iters}"
+    cells = []
+    for n_x, n_t in grids:
+        for m in m_values:
+            two, v = by[(n_x, n_t, m, "two_level")], by[(n_x, n_t, m, "v_cycle")]
+            cells.append(IterationCell(n_x, n_t, m, fmt(two), fmt(v), two, v))
     return cells
+
+
+def measured_points(family: str, p: int, coarse_kind: str, c_values: Sequence[float], m: int,
+                    n_x: int, n_t: int, config: Optional[mgrit.MgritConfig] = None,
+                    cycle: str = "two_level") -> List[mgrit.SolveReport]:
+    """``measured_point`` for many CFL numbers at once (the measured curve of
+    experiments.py:150-201, lfa_sweep(measure_grid=...)), solved concurrently
+    through ``mgrit.solve_many``; each report equals ``measured_point``'s."""
+    config = config or mgrit.MgritConfig()
+    if config.cycle != cycle:
+        config = mgrit.MgritConfig(config.nu, cycle, config.tol, config.max_iters,
+                                   config.rng_seed)
+    jobs = [(build_problem(DiscretizationSpec(family, p, c, n_x, n_t), m, cycle, coarse_kind),
+             config) for c in c_values]
+    return mgrit.solve_many(jobs)

@@ -221,8 +221,9 @@ def sequential_solve(problem: TimeGridProblem, level: int = 0, g=None):
 # ----------------------------------------------------------------- solver
 
 class _Level:
-    def __init__(self, torch, stepper: Stepper, m: int, n_pts: int, n_x: int, nu: int):
-        self.plan = plan_for(stepper.program)
+    def __init__(self, torch, stepper: Stepper, m: int, n_pts: int, n_x: int, nu: int,
+                 tag=None):
+        self.plan = plan_for(stepper.program, tag)
         self.m = m
         self.n_pts = n_pts
         self.n_int = (n_pts - 1) // m
@@ -241,6 +242,8 @@ class MgritSolver:
         self._built = False
         #: set to a list to record (name, start_event, end_event) per launch
         self.profile = None
+        #: plan tag: solvers that run concurrently (solve_many) get private plans
+        self.plan_tag = None
 
     # ---------------------------------------------------------- buffers
     def _build(self):
@@ -252,7 +255,7 @@ class MgritSolver:
         self._torch = torch
         nlev = len(pr.m)
         self.levels = [_Level(torch, pr.steppers[l], pr.m[l], pr.points_on_level(l), n_x,
-                              cfg.nu) for l in range(nlev)]
+                              cfg.nu, self.plan_tag) for l in range(nlev)]
         # coarse iterates e_l and right-hand sides g_l for levels 1..nlev
         self.ucoarse = [None]
         self.gcoarse = [None]
@@ -260,7 +263,7 @@ class MgritSolver:
             npts = pr.points_on_level(l)
             self.ucoarse.append(torch.zeros((npts, n_x), dtype=torch.float64, device="cuda"))
             self.gcoarse.append(torch.zeros((npts, n_x), dtype=torch.float64, device="cuda"))
-        self.plans = [plan_for(s.program) for s in pr.steppers]
+        self.plans = [plan_for(s.program, self.plan_tag) for s in pr.steppers]
         self.zero_row = torch.zeros(n_x, dtype=torch.float64, device="cuda")
         n0 = self.levels[0].n_int
         self.partials = torch.empty(max(n0, 1), dtype=torch.float64, device="cuda")
@@ -420,3 +423,86 @@ def solve(problem: TimeGridProblem, config: MgritConfig, threads: int = 1,
           initial_iterate=None) -> SolveReport:
     """Run MGRIT to the halting rule on the GPU (mgrit.py:288-291)."""
     return MgritSolver(problem, config, threads).solve(initial_iterate)
+
+
+def solve_many(jobs, streams: Optional[int] = None) -> List[SolveReport]:
+    """Many independent solves in flight at once (the Table-3 /
+    measured-point sweeps, experiments.py:190-242, are lists of small solves).
+
+    ``jobs``: sequence of ``(problem, config)`` or ``(problem, config,
+    initial_iterate)``.  Each solve gets its own CUDA stream (round-robin over
+    ``streams`` streams, default one per job), private device plans and
+    buffers, and runs exactly the kernel sequence of ``solve`` on that stream,
+    so every report is bitwise identical to the sequential one.  The host
+    drives the solves in lock step: it enqueues one cycle (plus the norm and an
+    asynchronous read-back of the squared norm) for every unfinished solve, then
+    reads the norms in order and applies each solve's halting rule
+    (mgrit.py:262-274).  Small problems occupy a few SMs each, so the cycles of
+    different solves run concurrently.  ``wall_time`` of a report is the time
+    from the start of the batch to that solve's halting decision."""
+    jobs = [tuple(j) for j in jobs]
+    if not jobs:
+        return []
+    torch = require_cuda()
+    ns = len(jobs) if not streams else max(1, min(int(streams), len(jobs)))
+    pool = [torch.cuda.Stream() for _ in range(ns)]
+    host = torch.zeros(len(jobs), dtype=torch.float64, pin_memory=True)
+    st = []
+    for i, job in enumerate(jobs):
+        problem, config = job[0], job[1]
+        init = job[2] if len(job) > 2 else None
+        s = pool[i % ns]
+        sol = MgritSolver(problem, config)
+        sol.plan_tag = ("stream", i % ns)
+        with torch.cuda.stream(s):
+            sol._build()
+            u = sol.initial_state() if init is None else init
+            ud, uh = to_device(u)
+        st.append(dict(sol=sol, stream=s, ud=ud, uh=uh, up=ptr(ud), norms=[], it=0,
+                       done=False, converged=False, ev=torch.cuda.Event(), wall=0.0))
+
+    def launch(k, first):
+        d = st[k]
+        sol = d["sol"]
+        with torch.cuda.stream(d["stream"]):
+            if first:
+                sol._residual_partials(d["up"], None)
+            else:
+                sol._cycle(0, d["up"], None, False, True)
+            device_sum(ptr(sol.partials), sol.levels[0].n_int, ptr(sol.sumbuf))
+            host[k:k + 1].copy_(sol.sumbuf, non_blocking=True)
+            d["ev"].record(d["stream"])
+
+    torch.cuda.synchronize()
+    start = time.perf_counter()
+    for k in range(len(st)):
+        launch(k, True)
+    active = list(range(len(st)))
+    while active:
+        nxt = []
+        for k in active:
+            d = st[k]
+            d["ev"].synchronize()
+            d["norms"].append(math.sqrt(float(host[k])))
+            cfg = d["sol"].config
+            n = d["norms"]
+            if len(n) > 1 and n[0] > 0 and n[-1] / n[0] <= cfg.tol:
+                d["converged"] = True
+            if d["converged"] or d["it"] >= cfg.max_iters:
+                d["done"] = True
+                d["wall"] = time.perf_counter() - start
+                continue
+            d["it"] += 1
+            launch(k, False)
+            nxt.append(k)
+        active = nxt
+    torch.cuda.synchronize()
+    out = []
+    for d in st:
+        d["sol"].last_iterate = d["ud"]
+        if d["uh"] is not None:
+            _writeback(d["uh"], d["ud"])
+        n = d["norms"]
+        rho = n[-1] / n[-2] if len(n) >= 2 and n[-2] > 0 else 0.0
+        out.append(SolveReport(n, d["it"], float(rho), d["converged"], d["wall"]))
+    return out
