@@ -160,6 +160,12 @@ class StepPlan:
     def handle(self):
         return self._h
 
+    def reserve(self, stream=None) -> None:
+        """Allocate the plan's lazily created workspace now (before a CUDA-graph
+        capture, which cannot allocate)."""
+        nat.check(self._lib.mgb_step_reserve_workspace(
+            self._h, stream if stream is not None else stream_handle()))
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:

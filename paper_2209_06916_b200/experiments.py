@@ -124,7 +124,8 @@ class IterationCell:
 def iteration_table(family: str, p: int, c: float, grids: Sequence[tuple],
                     m_values: Sequence[int], coarse_kind: str = "modified", nu: int = 1,
                     max_iters: int = 40, rng_seed: int = 0,
-                    threads: int = 1, concurrent: bool = False) -> List[IterationCell]:
+                    threads: int = 1, concurrent: bool = False,
+                    streams: Optional[int] = 8) -> List[IterationCell]:
     """Two-level and V-cycle iteration counts (experiments.py:221-242), on the GPU.
 
     ``concurrent=True`` (extension) runs every cell's solves at once through
@@ -140,7 +141,7 @@ def iteration_table(family: str, p: int, c: float, grids: Sequence[tuple],
                 keys.append((n_x, n_t, m, cycle))
                 jobs.append((build_problem(spec, m, cycle, coarse_kind), cfg))
     if concurrent:
-        reports = mgrit.solve_many(jobs)
+        reports = mgrit.solve_many(jobs, streams=streams)
     else:
         reports = [mgrit.solve(pr, cfg, threads=threads) for pr, cfg in jobs]
     by = dict(zip(keys, reports))
@@ -155,7 +156,7 @@ def iteration_table(family: str, p: int, c: float, grids: Sequence[tuple],
 
 def measured_points(family: str, p: int, coarse_kind: str, c_values: Sequence[float], m: int,
                     n_x: int, n_t: int, config: Optional[mgrit.MgritConfig] = None,
-                    cycle: str = "two_level") -> List[mgrit.SolveReport]:
+                    cycle: str = "two_level", streams: Optional[int] = 8) -> List[mgrit.SolveReport]:
     """``measured_point`` for many CFL numbers at once (the measured curve of
     experiments.py:150-201, lfa_sweep(measure_grid=...)), solved concurrently
     through ``mgrit.solve_many``; each report equals ``measured_point``'s."""
@@ -165,4 +166,4 @@ def measured_points(family: str, p: int, coarse_kind: str, c_values: Sequence[fl
                                    config.rng_seed)
     jobs = [(build_problem(DiscretizationSpec(family, p, c, n_x, n_t), m, cycle, coarse_kind),
              config) for c in c_values]
-    return mgrit.solve_many(jobs)
+    return mgrit.solve_many(jobs, streams=streams)

@@ -425,83 +425,124 @@ def solve(problem: TimeGridProblem, config: MgritConfig, threads: int = 1,
     return MgritSolver(problem, config, threads).solve(initial_iterate)
 
 
-def solve_many(jobs, streams: Optional[int] = None) -> List[SolveReport]:
+def solve_many(jobs, streams: Optional[int] = 8, graphs: bool = True,
+               l2_budget: Optional[float] = None) -> List[SolveReport]:
     """Many independent solves in flight at once (the Table-3 /
-    measured-point sweeps, experiments.py:190-242, are lists of small solves).
+    measured-point sweeps, experiments.py:150-242, are lists of small solves).
 
     ``jobs``: sequence of ``(problem, config)`` or ``(problem, config,
-    initial_iterate)``.  Each solve gets its own CUDA stream (round-robin over
-    ``streams`` streams, default one per job), private device plans and
-    buffers, and runs exactly the kernel sequence of ``solve`` on that stream,
-    so every report is bitwise identical to the sequential one.  The host
-    drives the solves in lock step: it enqueues one cycle (plus the norm and an
-    asynchronous read-back of the squared norm) for every unfinished solve, then
+    initial_iterate)``.  Up to ``streams`` solves are active at a time, each on
+    its own CUDA stream (slot) with private device plans and buffers, running
+    exactly the kernel sequence of ``solve``: every report (and iterate) is
+    bitwise identical to the sequential one.  Optionally a job is admitted to a
+    free slot only while the active iterates fit ``l2_budget`` bytes (always
+    when no other solve is active); measured on B200, concurrency beats L2
+    residency even for 1024 x 4096 Table-3 cells, so there is no budget by
+    default.  The host drives the active
+    solves in lock step: it enqueues one cycle (plus the norm and an
+    asynchronous read-back of the squared norm) for every active solve, then
     reads the norms in order and applies each solve's halting rule
-    (mgrit.py:262-274).  Small problems occupy a few SMs each, so the cycles of
-    different solves run concurrently.  ``wall_time`` of a report is the time
-    from the start of the batch to that solve's halting decision."""
+    (mgrit.py:262-274).  With ``graphs`` a solve's cycle + norm + read-back is
+    captured once as a CUDA graph and replayed per iteration (one launch
+    instead of ~15 host calls: small solves are launch-bound).  ``wall_time``
+    of a report is the time from the start of the batch to that solve's
+    halting decision."""
     jobs = [tuple(j) for j in jobs]
     if not jobs:
         return []
     torch = require_cuda()
-    ns = len(jobs) if not streams else max(1, min(int(streams), len(jobs)))
+    ns = max(1, min(int(streams or len(jobs)), len(jobs)))
     pool = [torch.cuda.Stream() for _ in range(ns)]
     host = torch.zeros(len(jobs), dtype=torch.float64, pin_memory=True)
     st = []
-    for i, job in enumerate(jobs):
-        problem, config = job[0], job[1]
-        init = job[2] if len(job) > 2 else None
-        s = pool[i % ns]
-        sol = MgritSolver(problem, config)
-        sol.plan_tag = ("stream", i % ns)
-        with torch.cuda.stream(s):
-            sol._build()
-            u = sol.initial_state() if init is None else init
-            ud, uh = to_device(u)
-        st.append(dict(sol=sol, stream=s, ud=ud, uh=uh, up=ptr(ud), norms=[], it=0,
-                       done=False, converged=False, ev=torch.cuda.Event(), wall=0.0))
+    for job in jobs:
+        problem = job[0]
+        st.append(dict(problem=problem, config=job[1], init=job[2] if len(job) > 2 else None,
+                       bytes=8.0 * (problem.n_t + 1) * problem.n_x, norms=[], it=0,
+                       converged=False, ev=torch.cuda.Event(), wall=0.0, graph=None))
 
-    def launch(k, first):
+    def enqueue(k, first):
         d = st[k]
         sol = d["sol"]
+        if first:
+            sol._residual_partials(d["up"], None)
+        else:
+            sol._cycle(0, d["up"], None, False, True)
+        device_sum(ptr(sol.partials), sol.levels[0].n_int, ptr(sol.sumbuf))
+        host[k:k + 1].copy_(sol.sumbuf, non_blocking=True)
+
+    def start_job(k, slot):
+        d = st[k]
+        sol = MgritSolver(d["problem"], d["config"])
+        sol.plan_tag = ("slot", slot)
+        d.update(sol=sol, slot=slot, stream=pool[slot])
+        with torch.cuda.stream(pool[slot]):
+            sol._build()
+            u = sol.initial_state() if d["init"] is None else d["init"]
+            d["ud"], d["uh"] = to_device(u)
+            d["up"] = ptr(d["ud"])
+            if graphs:
+                for plan in [L.plan for L in sol.levels] + sol.plans:
+                    plan.reserve()
+                g = torch.cuda.CUDAGraph()
+                g.capture_begin(capture_error_mode="thread_local")
+                try:
+                    enqueue(k, False)
+                finally:
+                    g.capture_end()
+                d["graph"] = g
+            enqueue(k, True)
+            d["ev"].record(pool[slot])
+
+    def next_cycle(k):
+        d = st[k]
         with torch.cuda.stream(d["stream"]):
-            if first:
-                sol._residual_partials(d["up"], None)
+            if d["graph"] is not None:
+                d["graph"].replay()
             else:
-                sol._cycle(0, d["up"], None, False, True)
-            device_sum(ptr(sol.partials), sol.levels[0].n_int, ptr(sol.sumbuf))
-            host[k:k + 1].copy_(sol.sumbuf, non_blocking=True)
+                enqueue(k, False)
             d["ev"].record(d["stream"])
+
+    def finish(d):
+        d["sol"].last_iterate = d["ud"]
+        if d["uh"] is not None:
+            with torch.cuda.stream(d["stream"]):
+                _writeback(d["uh"], d["ud"])
+        d["graph"] = None
 
     torch.cuda.synchronize()
     start = time.perf_counter()
-    for k in range(len(st)):
-        launch(k, True)
-    active = list(range(len(st)))
-    while active:
+    pending = list(range(len(st)))
+    active, free = [], list(range(ns))
+    while pending or active:
+        load = sum(st[k]["bytes"] for k in active)
+        while pending and free and (not active or l2_budget is None
+                                    or load + st[pending[0]]["bytes"] <= l2_budget):
+            k = pending.pop(0)
+            start_job(k, free.pop(0))
+            active.append(k)
+            load += st[k]["bytes"]
         nxt = []
         for k in active:
             d = st[k]
             d["ev"].synchronize()
-            d["norms"].append(math.sqrt(float(host[k])))
-            cfg = d["sol"].config
             n = d["norms"]
+            n.append(math.sqrt(float(host[k])))
+            cfg = d["config"]
             if len(n) > 1 and n[0] > 0 and n[-1] / n[0] <= cfg.tol:
                 d["converged"] = True
             if d["converged"] or d["it"] >= cfg.max_iters:
-                d["done"] = True
                 d["wall"] = time.perf_counter() - start
+                finish(d)
+                free.append(d["slot"])
                 continue
             d["it"] += 1
-            launch(k, False)
+            next_cycle(k)
             nxt.append(k)
         active = nxt
     torch.cuda.synchronize()
     out = []
     for d in st:
-        d["sol"].last_iterate = d["ud"]
-        if d["uh"] is not None:
-            _writeback(d["uh"], d["ud"])
         n = d["norms"]
         rho = n[-1] / n[-2] if len(n) >= 2 and n[-2] > 0 else 0.0
         out.append(SolveReport(n, d["it"], float(rho), d["converged"], d["wall"]))
