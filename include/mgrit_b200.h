@@ -126,6 +126,15 @@ int mgb_relax(mgb_step* step, const mgb_relax_args* args, void* stream);
  * Backs np.linalg.norm in cpoint_residual_norm (mgrit.py:164-166). */
 int mgb_sum(const double* partials, int64_t n, double* out, void* stream);
 
+/* Strided row copy (any direction, UVA): `rows` rows of `row_bytes` bytes from
+ * src (row pitch src_pitch bytes) to dst (pitch dst_pitch), asynchronous on
+ * `stream`.  Moves the live rows of a host iterate to the device in one DMA
+ * (solve(initial_iterate=<host>), mgrit.py:288-291): only the C-points and
+ * the rows before them are read before the first closing F-relaxation
+ * rewrites every F-point. */
+int mgb_copy_rows(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                  int64_t row_bytes, int64_t rows, void* stream);
+
 /* Diagnostics: launch the FP64 (DFMA) throughput probe used as the FP64
  * roofline denominator by bench.py; *flops_per_launch receives its flop count. */
 int mgb_fp64_peak(int64_t iters, double* flops_per_launch, void* stream);

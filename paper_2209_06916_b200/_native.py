@@ -54,7 +54,7 @@ class RelaxArgs(ctypes.Structure):
 #: every symbol the header declares (checked by tests/test_native_abi.py)
 EXPORTED = ("mgb_step_create", "mgb_step_destroy", "mgb_step_layout",
             "mgb_step_reserve_workspace", "mgb_relax", "mgb_sum", "mgb_version",
-            "mgb_last_error", "mgb_launch_count", "mgb_fp64_peak")
+            "mgb_last_error", "mgb_launch_count", "mgb_fp64_peak", "mgb_copy_rows")
 
 _lib: Optional[ctypes.CDLL] = None
 
@@ -92,6 +92,9 @@ def load() -> ctypes.CDLL:
     lib.mgb_launch_count.restype = _i64
     lib.mgb_fp64_peak.argtypes = [_i64, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
     lib.mgb_fp64_peak.restype = _i32
+    lib.mgb_copy_rows.argtypes = [ctypes.c_void_p, _i64, ctypes.c_void_p, _i64, _i64, _i64,
+                                  ctypes.c_void_p]
+    lib.mgb_copy_rows.restype = _i32
     _lib = lib
     return lib
 

@@ -848,6 +848,16 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   return MGB_OK;
 }
 
+int mgb_copy_rows(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                  int64_t row_bytes, int64_t rows, void* stream) {
+  if (rows <= 0 || row_bytes <= 0) return MGB_OK;
+  if (!dst || !src) return fail(MGB_ERR_INVALID, "null pointer");
+  if (dst_pitch < row_bytes || src_pitch < row_bytes) return fail(MGB_ERR_INVALID, "pitch < row bytes");
+  CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)dst_pitch, src, (size_t)src_pitch, (size_t)row_bytes,
+                             (size_t)rows, cudaMemcpyDefault, (cudaStream_t)stream));
+  return MGB_OK;
+}
+
 int mgb_sum(const double* partials, int64_t n, double* out, void* stream) {
   if (!out) return fail(MGB_ERR_INVALID, "null out");
   if (n <= 0) {

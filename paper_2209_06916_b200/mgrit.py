@@ -30,7 +30,12 @@ from typing import List, Optional
 
 import numpy as np
 
-from .device import device_sum, plan_for, ptr, require_cuda, to_device
+from . import _native
+from .device import device_sum, is_tensor, plan_for, ptr, require_cuda, stream_handle, to_device
+
+nat_load, nat_check = _native.load, _native.check
+#: tests: fill the rows ``MgritSolver._upload`` does not copy with NaN
+POISON_SKIPPED_ROWS = False
 from .stepping import Stepper
 
 _F64 = 8
@@ -393,9 +398,10 @@ class MgritSolver:
         self._build()
         torch = self._torch
         cfg = self.config
-        if u is None:
+        internal = u is None
+        if internal:
             u = self.initial_state()
-        ud, uh = to_device(u)
+        ud, uh = self._upload(u)
         up = ptr(ud)
         torch.cuda.synchronize()
         start = time.perf_counter()
@@ -413,10 +419,54 @@ class MgritSolver:
         torch.cuda.synchronize()
         wall = time.perf_counter() - start
         self.last_iterate = ud
-        if uh is not None:
+        if uh is not None and not internal:  # in-place semantics for a caller's array
             _writeback(uh, ud)
         rho = norms[-1] / norms[-2] if len(norms) >= 2 and norms[-2] > 0 else 0.0
         return SolveReport(norms, it, float(rho), converged, wall)
+
+    def _upload(self, u):
+        """Device copy of a host iterate for ``solve``: only the rows the solve
+        reads before rewriting them -- the C-points u[km] and the rows
+        u[km-1] before them (initial residual, mgrit.py:164-166 / 259-261; the
+        first FC pass reads the C-points) -- travel, as two strided DMAs.  The
+        first closing F-relaxation (mgrit.py:247; the fused CF pass) rewrites
+        every F-point before any is read, so the other rows of the initial
+        iterate cannot influence the result (tests/test_gpu_parity.py checks
+        host and device inputs give bitwise identical solves, with the
+        skipped rows poisoned).  CUDA tensors are used in place."""
+        torch = self._torch
+        pr = self.problem
+        m = pr.m[0] if pr.m else 0
+        self.last_upload_bytes = 0
+        if is_tensor(u) and u.is_cuda:
+            return to_device(u)
+        if m < 3:
+            self.last_upload_bytes = 8 * (pr.n_t + 1) * pr.n_x
+            return to_device(u)
+        shape = (pr.n_t + 1, pr.n_x)
+        if is_tensor(u):
+            if u.dtype != torch.float64:
+                raise TypeError("device arrays must be float64")
+            src = u.contiguous().reshape(shape)
+        else:
+            arr = np.asarray(u)
+            if np.iscomplexobj(arr):
+                raise NotImplementedError("complex arrays are not supported on the device path")
+            src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64).reshape(shape))
+        ud = torch.empty(shape, dtype=torch.float64, device="cuda")
+        if POISON_SKIPPED_ROWS:
+            ud.fill_(float("nan"))
+        row = pr.n_x * _F64
+        n_int = pr.n_t // m
+        h, d = src.data_ptr(), ud.data_ptr()
+        lib, stream = nat_load(), stream_handle()
+        nat_check(lib.mgb_copy_rows(d, m * row, h, m * row, row, n_int + 1, stream))
+        nat_check(lib.mgb_copy_rows(d + (m - 1) * row, m * row, h + (m - 1) * row, m * row, row,
+                                    n_int, stream))
+        self.last_upload_bytes = (2 * n_int + 1) * row
+        if not (is_tensor(u) and u.is_pinned()):
+            torch.cuda.current_stream().synchronize()  # pageable source: keep it alive
+        return ud, u
 
 
 def solve(problem: TimeGridProblem, config: MgritConfig, threads: int = 1,

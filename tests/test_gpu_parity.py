@@ -305,3 +305,34 @@ def test_time_sharded_engine_single_rank_matches_solver():
         np.testing.assert_allclose(rep.residual_norms, ref.residual_norms, rtol=1e-14)
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------ host-iterate upload (solve)
+
+@pytest.mark.parametrize("fam,p,c,n_x,n_t,m,cyc", [("erk", 3, 0.85, 256, 1024, 8, "v_cycle"),
+                                                   ("erk", 1, 0.85, 128, 256, 4, "two_level"),
+                                                   ("sdirk", 3, 4.0, 128, 256, 4, "v_cycle")])
+def test_host_iterate_upload_of_live_rows_only(fam, p, c, n_x, n_t, m, cyc, monkeypatch):
+    """solve(initial_iterate=<host>) copies only the C-points and the rows before
+    them; the skipped rows are poisoned with NaN and the solve must still equal
+    (bitwise) the solve of the same iterate given as a CUDA tensor, and write
+    the full final iterate back in place (mgrit.py:288-291)."""
+    import torch
+    from paper_2209_06916_b200 import mgrit as M
+    monkeypatch.setattr(M, "POISON_SKIPPED_ROWS", True)
+    prob = P.experiments.build_problem(P.DiscretizationSpec(fam, p, c, n_x, n_t), m, cyc, "modified")
+    cfg = P.MgritConfig(cycle=cyc)
+    u0 = P.MgritSolver(prob, cfg).initial_state()
+    dev = torch.from_numpy(u0.copy()).cuda()
+    r_dev = P.solve(prob, cfg, initial_iterate=dev)
+    host_np = u0.copy()
+    r_np = P.solve(prob, cfg, initial_iterate=host_np)
+    host_t = torch.from_numpy(u0.copy()).pin_memory()
+    r_t = P.solve(prob, cfg, initial_iterate=host_t)
+    for r in (r_np, r_t):
+        assert r.residual_norms == r_dev.residual_norms and r.iterations == r_dev.iterations
+    ref = dev.cpu().numpy()
+    assert np.array_equal(host_np, ref) and np.array_equal(host_t.numpy(), ref)
+    assert not np.isnan(ref).any()
+    # default solve (internal iterate) gives the same history
+    assert P.solve(prob, cfg).residual_norms == r_dev.residual_norms
