@@ -21,8 +21,10 @@ BASELINE workload; value = n_x * n_t / (time per solve), whole job.
 * --impl reference: the same oracle as the reference arm (the reference is
   pure Python/numpy; /root/reference is absent on the GPU box).
 Multi-GPU (torchrun, N > 1): ONE time-sharded solve of the workload over the N
-ranks (strong scaling): level-0 interval blocks per rank, boundary C-point rows
-and the coarse right-hand side exchanged over NCCL, coarse levels on rank 0
+ranks (strong scaling): every level whose intervals split over the ranks is
+sharded in contiguous interval blocks, one boundary C-point row per FC pass and
+level goes to the right neighbour over NCCL, the first level with too few
+intervals is gathered to rank 0 with the rest of the cycle
 (paper_2209_06916_b200/distributed.py).
 """
 
@@ -328,8 +330,9 @@ def run_gpu(args):
 
 def run_sharded(args, cf, prob, cfg, rank, world, local):
     """N > 1: one time-sharded solve of the workload over all ranks (strong
-    scaling): level-0 interval blocks per rank, boundary-row exchange and coarse
-    gather over NCCL, coarse levels on rank 0 (paper_2209_06916_b200/distributed.py)."""
+    scaling): interval blocks per rank on every sharded level, boundary-row
+    exchange over NCCL, the remaining coarse levels on rank 0
+    (paper_2209_06916_b200/distributed.py)."""
     import torch
     import torch.distributed as dist
     from paper_2209_06916_b200 import _native
@@ -389,8 +392,8 @@ def run_sharded(args, cf, prob, cfg, rank, world, local):
         "config": {"workload": f"{cf.name}: {cf.family.upper()}{cf.p}+U{cf.p} c={cf.c} "
                                f"n_x={cf.n_x} n_t={cf.n_t} m={cf.m} {cf.cycle}",
                    "iterations": rep.iterations, "converged": rep.converged,
-                   "parallelism": f"time-sharded x{world} (level-0 interval blocks, "
-                                  f"coarse levels on rank 0)"},
+                   "parallelism": f"time-sharded x{world} (levels 0..{sol.ls - 1} in interval "
+                                  f"blocks per rank, levels >= {sol.ls} on rank 0)"},
         "e2e": {"value": dof / float(te.item()), "unit": "DOF/s",
                 "h2d_bytes_per_step": int(nbytes.item()),
                 "d2h_bytes_per_step": int(nbytes.item())},

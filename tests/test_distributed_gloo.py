@@ -1,7 +1,8 @@
-"""Time-sharded MGRIT host logic on CPU (gloo, world_size 1 and 2) with a
-numpy engine built on the oracle: the sharded iterate must equal the
-single-process oracle iterate BIT FOR BIT, and the residual history must be
-bitwise identical for 1 and 2 ranks (fixed-order norm reduction)."""
+"""Time-sharded MGRIT host logic on CPU (gloo, world_size 1, 2 and 4) with a
+numpy engine built on the oracle: every level with enough intervals is
+sharded; the sharded iterate must equal the single-process oracle iterate BIT
+FOR BIT, and the residual history must be bitwise identical for any rank count
+(fixed-order norm reduction).  Covers two-level, V- and F-cycles, nu = 0/1/2."""
 
 import os
 import socket
@@ -17,19 +18,24 @@ from oracle import mgrit_oracle as O
 from paper_2209_06916_b200.distributed import Engine, ShardedMgritSolver, block_of
 from paper_2209_06916_b200.mgrit import MgritConfig
 
-CASES = {
-    "erk1_two_level": ("erk", 1, 0.85, 64, 128, 8, "two_level"),
-    "erk3_v_cycle": ("erk", 3, 0.85, 64, 256, 4, "v_cycle"),
-    "sdirk3_v_cycle": ("sdirk", 3, 4.0, 64, 256, 4, "v_cycle"),
+CASES = {  # family, p, c, n_x, n_t, m, cycle, nu
+    "erk1_two_level": ("erk", 1, 0.85, 64, 128, 8, "two_level", 1),
+    "erk3_v_cycle": ("erk", 3, 0.85, 64, 256, 4, "v_cycle", 1),
+    "sdirk3_v_cycle": ("sdirk", 3, 4.0, 64, 256, 4, "v_cycle", 1),
+    "erk3_f_cycle": ("erk", 3, 0.85, 64, 256, 4, "f_cycle", 1),
+    "erk1_v_nu0": ("erk", 1, 0.85, 32, 256, 2, "v_cycle", 0),
+    "erk3_v_nu2": ("erk", 3, 0.85, 32, 256, 4, "v_cycle", 2),
 }
 
 
 class OracleEngine(Engine):
-    """Rank-local level-0 passes restated with the numpy oracle (test only)."""
+    """Rank-local passes of every level restated with the numpy oracle, with
+    the oracle's operation order (mgrit_oracle.f_relax / c_relax / restrict /
+    cycle_once) -- test only."""
 
-    def __init__(self, steps, factors, n_t, u0, cycle):
-        self.steps, self.factors, self.n_t, self.u0, self.cycle = steps, factors, n_t, u0, cycle
-        self.step, self.m, self.n = steps[0], factors[0], len(u0)
+    def __init__(self, steps, factors, n_t, u0, nu):
+        self.steps, self.factors, self.n_t, self.u0, self.nu = steps, factors, n_t, u0, nu
+        self.n = len(u0)
 
     def zeros(self, rows):
         return np.zeros((rows, self.n))
@@ -40,61 +46,98 @@ class OracleEngine(Engine):
     def from_comm(self, t, like):
         return t.numpy()
 
-    def _fsweep(self, X):
-        for _ in range(self.m - 1):
-            X = self.step.apply(X) + 0.0  # upd + g, g = 0 on the fine level
+    def _g(self, g, j, m, nb):
+        return 0.0 if g is None else g[j:nb * m + 1:m][:nb]
+
+    def _start(self, l, u, src, k0, nb, u_zero):
+        m = self.factors[l]
+        if src is None:
+            C = np.zeros((nb, self.n)) if u_zero else u[0:nb * m:m].copy()
+        else:
+            C = src[:nb].copy()
+        if k0 == 0:
+            C[0] = 0.0 if u_zero else u[0]
+        return C
+
+    def _fsweep(self, l, X, g, nb):
+        m = self.factors[l]
+        for j in range(1, m):
+            X = self.steps[l].apply(X) + self._g(g, j, m, nb)
         return X
 
     def initial_partials(self, u_loc, nb):
-        m = self.m
-        r = (0.0 + self.step.apply(u_loc[m - 1::m][:nb])) - u_loc[m::m][:nb]
+        m, st = self.factors[0], self.steps[0]
+        r = (0.0 + st.apply(u_loc[m - 1::m][:nb])) - u_loc[m::m][:nb]
         return np.array([float(np.dot(x, x)) for x in r])
 
-    def fc(self, u_loc, cb, k0, nb):
-        cb[1:] = self.step.apply(self._fsweep(u_loc[0:nb * self.m:self.m].copy())) + 0.0
+    def fc(self, l, u, g, src, cb, k0, nb, u_zero):
+        m = self.factors[l]
+        X = self._fsweep(l, self._start(l, u, src, k0, nb, u_zero), g, nb)
+        cb[1:nb + 1] = self.steps[l].apply(X) + self._g(g, m, m, nb)
 
-    def fr(self, cb, g1, k0, nb):
-        g1[:] = (0.0 + self.step.apply(self._fsweep(cb[:nb].copy()))) - cb[1:]
+    def fr(self, l, u, g, src, gn, k0, nb, u_zero):
+        m = self.factors[l]
+        X = self._fsweep(l, self._start(l, u, src, k0, nb, u_zero), g, nb)
+        if src is None:
+            cref = np.zeros((nb, self.n)) if u_zero else u[m:nb * m + 1:m]
+        else:
+            cref = src[1:nb + 1]
+        gn[1:nb + 1] = (self._g(g, m, m, nb) + self.steps[l].apply(X)) - cref
 
-    def cf(self, u_loc, cb, e_loc, k0, nb):
-        m = self.m
-        c = cb[:nb].copy()
-        start = 1 if k0 == 0 else 0
-        c[start:] = cb[start:nb] + e_loc[start:nb]
-        u_loc[0:nb * m:m] = c
-        X = c
+    def cf(self, l, u, g, src, e, k0, nb, u_zero, want_norm):
+        m, st = self.factors[l], self.steps[l]
+        if src is None:
+            base = np.zeros((nb + 1, self.n)) if u_zero else u[0:nb * m + 1:m].copy()
+        else:
+            base = src[:nb + 1].copy()
+        C = base + e[:nb + 1]
+        if k0 == 0:
+            C[0] = 0.0 if u_zero else u[0]
+        u[0:nb * m:m] = C[:nb]
+        X = C[:nb]
         for j in range(1, m):
-            X = self.step.apply(X) + 0.0
-            u_loc[j:nb * m:m] = X
-        u_loc[nb * m] = cb[nb] + e_loc[nb]
-        r = (0.0 + self.step.apply(X)) - (cb[1:] + e_loc[1:])
+            X = st.apply(X) + self._g(g, j, m, nb)
+            u[j:nb * m:m] = X
+        u[nb * m] = C[nb]
+        if not want_norm:
+            return None
+        r = (self._g(g, m, m, nb) + st.apply(X)) - C[1:nb + 1]
         return np.array([float(np.dot(x, x)) for x in r])
 
-    def coarse_solve(self, gc):
-        if self.cycle == "two_level" or len(self.factors) == 1:
-            return O.forward_substitute(self.steps[1], gc)
-        mg = O.Mgrit(self.steps, self.factors, self.n_t, self.u0, cycle=self.cycle)
+    def coarse_solve(self, level, gc, kind):
+        if kind == "two_level" or level == len(self.factors):
+            return O.forward_substitute(self.steps[level], gc)
+        mg = O.Mgrit(self.steps, self.factors, self.n_t, self.u0, nu=self.nu, cycle=kind)
         e = np.zeros_like(gc)
-        mg.cycle_once(1, e, gc)
+        if kind == "f_cycle":
+            mg.cycle_once(level, e, gc, "f_cycle")
+            mg.cycle_once(level, e, gc, "v_cycle")
+        else:
+            mg.cycle_once(level, e, gc, "v_cycle")
         return e
 
 
-def _worker(rank, world, port, case, outdir):
+def _hier(case):
+    fam, p, c, nx, nt, m, cyc, nu = CASES[case]
+    return O.build_hierarchy(fam, p, c, nx, nt, m, "v_cycle" if cyc == "f_cycle" else cyc,
+                             fine_mode="staged" if fam == "sdirk" else "assembled")
+
+
+def _worker(rank, world, port, case, outdir, max_sharded):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    fam, p, c, nx, nt, m, cyc = CASES[case]
-    steps, fac, u0 = O.build_hierarchy(fam, p, c, nx, nt, m, cyc,
-                                       fine_mode="staged" if fam == "sdirk" else "assembled")
+    fam, p, c, nx, nt, m, cyc, nu = CASES[case]
+    steps, fac, u0 = _hier(case)
     u = O.initial_iterate(0, nt, nx, u0)
-    eng = OracleEngine(steps, fac, nt, u0, cyc)
+    eng = OracleEngine(steps, fac, nt, u0, nu)
     # a problem object only for metadata (m, n_t) -- the engine does the work
     prob = type("Prob", (), {"m": fac, "n_t": nt, "n_x": nx})()
-    sol = ShardedMgritSolver(prob, MgritConfig(cycle=cyc), eng)
+    sol = ShardedMgritSolver(prob, MgritConfig(cycle=cyc, nu=nu), eng, max_sharded=max_sharded)
     r0, r1 = sol.local_rows()
     u_loc = u[r0:r1].copy()
     rep = sol.solve(u_loc)
     np.savez(os.path.join(outdir, f"{case}_{world}_{rank}.npz"), u=u_loc, r0=r0,
-             norms=np.array(rep.residual_norms), iters=rep.iterations)
+             norms=np.array(rep.residual_norms), iters=rep.iterations, ls=sol.ls)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -107,27 +150,54 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("case", sorted(CASES))
-def test_sharded_matches_single_process_oracle(case):
-    fam, p, c, nx, nt, m, cyc = CASES[case]
-    steps, fac, u0 = O.build_hierarchy(fam, p, c, nx, nt, m, cyc,
-                                       fine_mode="staged" if fam == "sdirk" else "assembled")
-    ref = O.Mgrit(steps, fac, nt, u0, cycle=cyc).solve()
+def _run(case, worlds, max_sharded=None):
+    fam, p, c, nx, nt, m, cyc, nu = CASES[case]
     with tempfile.TemporaryDirectory() as d:
         runs = {}
-        for world in (1, 2):
-            mp.spawn(_worker, args=(world, _free_port(), case, d), nprocs=world, join=True)
+        for world in worlds:
+            mp.spawn(_worker, args=(world, _free_port(), case, d, max_sharded), nprocs=world,
+                     join=True)
             parts = [np.load(os.path.join(d, f"{case}_{world}_{r}.npz")) for r in range(world)]
-            u = ref["u"].copy() * np.nan
+            u = np.full((nt + 1, nx), np.nan)
             for q in parts:
                 r0 = int(q["r0"])
                 u[r0:r0 + q["u"].shape[0]] = q["u"]
-            runs[world] = (u, parts[0]["norms"], int(parts[0]["iters"]))
-    for world, (u, norms, iters) in runs.items():
+            runs[world] = (u, parts[0]["norms"], int(parts[0]["iters"]), int(parts[0]["ls"]))
+    return runs
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_sharded_matches_single_process_oracle(case):
+    """Every level with enough intervals is sharded (1, 2 and 4 ranks); the
+    assembled iterate equals the single-process oracle bit for bit."""
+    fam, p, c, nx, nt, m, cyc, nu = CASES[case]
+    steps, fac, u0 = _hier(case)
+    ref = O.Mgrit(steps, fac, nt, u0, nu=nu, cycle=cyc).solve()
+    runs = _run(case, (1, 2, 4))
+    for world, (u, norms, iters, ls) in runs.items():
         assert iters == ref["iterations"]
         assert np.array_equal(u, ref["u"]), world            # bit-identical iterate
         np.testing.assert_allclose(norms, ref["norms"], rtol=1e-13, atol=0)
-    assert np.array_equal(runs[1][1], runs[2][1])               # bitwise across rank counts
+    for world in (2, 4):
+        assert np.array_equal(runs[1][1], runs[world][1])    # bitwise across rank counts
+    if cyc != "two_level":
+        assert runs[2][3] >= 2                               # coarse levels sharded too
+
+
+def test_level0_only_sharding_equals_multilevel():
+    """max_sharded=1 (gather right after level 0) gives the same iterate."""
+    a = _run("erk3_v_cycle", (2,), max_sharded=1)[2]
+    b = _run("erk3_v_cycle", (2,))[2]
+    assert a[3] == 1 and b[3] > 1
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_sharded_level_count():
+    from paper_2209_06916_b200.distributed import sharded_levels
+    assert sharded_levels([8, 8, 8, 8], 16384, 8, "v_cycle") == 3   # cfg2: L3 (4 intervals) on rank 0
+    assert sharded_levels([8, 8, 8, 8], 16384, 2, "v_cycle") == 4
+    assert sharded_levels([8] * 6, 2 ** 20, 8, "v_cycle") == 5       # cfg5
+    assert sharded_levels([8], 1024, 4, "two_level") == 1
 
 
 def test_initial_rows_match_one_shot_rng():

@@ -282,9 +282,17 @@ def test_baseline_config_against_reference_history(name):
     assert dev <= _TOL[name], dev
 
 
-def test_time_sharded_engine_single_rank_matches_solver():
-    """The NCCL time-sharded driver (GpuEngine) on one rank reproduces the
-    single-GPU solver bit for bit (multi-rank logic: tests/test_distributed_gloo.py)."""
+@pytest.mark.parametrize("fam,p,c,n_x,n_t,m,cyc,nu,max_sharded", [
+    ("erk", 3, 0.85, 256, 1024, 8, "v_cycle", 1, None),
+    ("erk", 3, 0.85, 256, 1024, 8, "v_cycle", 1, 1),
+    ("sdirk", 3, 4.0, 128, 1024, 4, "v_cycle", 1, None),
+    ("erk", 3, 0.85, 128, 1024, 4, "f_cycle", 2, None),
+    ("erk", 1, 0.85, 128, 256, 4, "two_level", 0, None)])
+def test_time_sharded_engine_single_rank_matches_solver(fam, p, c, n_x, n_t, m, cyc, nu,
+                                                        max_sharded):
+    """The NCCL time-sharded driver (GpuEngine, every level sharded) on one rank
+    reproduces the single-GPU solver bit for bit (multi-rank logic:
+    tests/test_distributed_gloo.py)."""
     import socket
     import torch
     import torch.distributed as dist
@@ -292,14 +300,16 @@ def test_time_sharded_engine_single_rank_matches_solver():
     s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     try:
-        spec = P.DiscretizationSpec("erk", 3, 0.85, 256, 1024)
-        prob = P.experiments.build_problem(spec, 8, "v_cycle")
-        cfg = P.MgritConfig(cycle="v_cycle")
-        u = O.initial_iterate(0, 1024, 256, prob.u0)
+        spec = P.DiscretizationSpec(fam, p, c, n_x, n_t)
+        prob = P.experiments.build_problem(spec, m, "v_cycle" if cyc == "f_cycle" else cyc)
+        cfg = P.MgritConfig(cycle=cyc, nu=nu)
+        u = O.initial_iterate(0, n_t, n_x, prob.u0)
         ref_u = u.copy()
         ref = P.solve(prob, cfg, initial_iterate=ref_u)
         ud = torch.from_numpy(u).cuda()
-        rep = ShardedMgritSolver(prob, cfg, GpuEngine(prob, cfg)).solve(ud)
+        sol = ShardedMgritSolver(prob, cfg, GpuEngine(prob, cfg), max_sharded=max_sharded)
+        rep = sol.solve(ud)
+        assert sol.ls == (1 if (max_sharded == 1 or cyc == "two_level") else len(prob.m))
         assert rep.iterations == ref.iterations
         assert np.array_equal(ud.cpu().numpy(), ref_u)
         np.testing.assert_allclose(rep.residual_norms, ref.residual_norms, rtol=1e-14)
