@@ -47,6 +47,12 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK_GBS = 6650.0
 
 
+def workload(cf) -> str:
+    """The workload named in every bench line (both arms, every N)."""
+    return (f"{cf.name}: {cf.family.upper()}{cf.p}+U{cf.p} c={cf.c} n_x={cf.n_x} n_t={cf.n_t} "
+            f"m={cf.m} {cf.cycle} {cf.coarse} coarse op, FCF, tol 1e-10, u0={cf.u0}")
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -295,10 +301,8 @@ def run_gpu(args):
         "metric": "MGRIT time-to-tolerance fine space-time DOF/s (FP64)",
         "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cf.name}: {cf.family.upper()}{cf.p}+U{cf.p} c={cf.c} "
-                               f"n_x={cf.n_x} n_t={cf.n_t} m={cf.m} {cf.cycle} "
-                               f"{cf.coarse} coarse op, FCF, tol 1e-10, u0={cf.u0}",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload(cf),
                    "iterations": rep.iterations, "converged": rep.converged,
                    "final_ratio": rep.residual_norms[-1] / rep.residual_norms[0],
                    "time_to_tolerance_s": ms_step / 1e3,
@@ -389,8 +393,7 @@ def run_sharded(args, cf, prob, cfg, rank, world, local):
         "value": dof / (ms_step / 1e3), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cf.name}: {cf.family.upper()}{cf.p}+U{cf.p} c={cf.c} "
-                               f"n_x={cf.n_x} n_t={cf.n_t} m={cf.m} {cf.cycle}",
+        "config": {"workload": workload(cf),
                    "iterations": rep.iterations, "converged": rep.converged,
                    "parallelism": f"time-sharded x{world} (levels 0..{sol.ls - 1} in interval "
                                   f"blocks per rank, levels >= {sol.ls} on rank 0)"},
@@ -452,13 +455,14 @@ def run_reference(args):
     value = cf.n_x * cf.n_t / per_solve
     sample = (f"numpy oracle: each step = 1 FCF iteration (+ initial norm) of {cf.name} at full "
               f"size; {len(times)} of {args.steps} steps run (180 s budget); extrapolated "
-              f"x {iters} iterations (the oracle's own count)")
+              f"x {iters} iterations (the reference's own count); threads=1, the reference's "
+              f"fastest setting (its row-chunk thread pool is GIL-bound and slower, SURVEY 6.2)")
     print(json.dumps({
         "impl": "reference", "metric": "MGRIT time-to-tolerance fine space-time DOF/s (FP64)",
         "value": value, "unit": "DOF/s", "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
         "steps": len(times), "warmup": 0, "ms_per_step": per_solve * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cf.name},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": workload(cf)},
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
