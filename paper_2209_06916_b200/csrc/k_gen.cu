@@ -14,6 +14,10 @@ void register_gen() {
                   reinterpret_cast<const void*>(&relax_kernel<16, K_SLG, 0, 1, true, 256>));
   register_kernel(KernelKey{K_SLG, 8, 0, 2, 1},
                   reinterpret_cast<const void*>(&relax_kernel<8, K_SLG, 0, 1, true, 256>));
+  // 2 CTAs/SM variant (<= 128 registers, parameter prefix only in shared memory)
+  // for many-interval levels that would otherwise need two waves (key: nst = 3)
+  register_kernel(KernelKey{K_SLG, 16, 0, 3, 1},
+                  reinterpret_cast<const void*>(&relax_kernel<16, K_SLG, 0, 1, true, 256, 2>));
   GEN_P(1)
   GEN_P(2)
   GEN_P(4)

@@ -911,13 +911,24 @@ __device__ __forceinline__ void step_once(Ctx& c, const double (&wd)[SPAN + 1], 
 __host__ __device__ constexpr int sp_bytes() { return (int)sizeof(StepParams); }
 
 // MAXT: launch bound (512, or 256 for register-heavy GMRES variants, T <= 256)
-template <int P, int KIND, int SPAN, int NST, bool EXACT, int MAXT = 512>
-__global__ void __launch_bounds__(MAXT) relax_kernel(const StepParams* __restrict__ gp, const RelaxLaunch L) {
+// Shared-memory copy of the step parameters: the whole StepParams, or for the
+// 2-CTA/SM single-CTA GMRES variant only the prefix before the factor tables
+// (which GMRES plans do not use), so two CTAs' slices + TMA stages fit an SM.
+template <int KIND, int MINB>
+__host__ __device__ constexpr int sp_smem_bytes() {
+  return (KIND == K_SLG && MINB > 1) ? (int)((offsetof(StepParams, fac) + 15) / 16 * 16)
+                                     : (int)sizeof(StepParams);
+}
+
+template <int P, int KIND, int SPAN, int NST, bool EXACT, int MAXT = 512, int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __restrict__ gp,
+                                                           const RelaxLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int SPB = sp_smem_bytes<KIND, MINB>();
   {
     const int4* src = reinterpret_cast<const int4*>(gp);
     int4* dst = reinterpret_cast<int4*>(smem_raw);
-    for (int i = threadIdx.x; i < (int)(sizeof(StepParams) / 16); i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < SPB / 16; i += blockDim.x) dst[i] = src[i];
   }
   __syncthreads();
   const StepParams& sp = *reinterpret_cast<const StepParams*>(smem_raw);
@@ -929,7 +940,7 @@ __global__ void __launch_bounds__(MAXT) relax_kernel(const StepParams* __restric
   c.S = sp.S;
   c.t = threadIdx.x;
   c.own = c.t < c.T;
-  c.row = reinterpret_cast<double*>(smem_raw + sizeof(StepParams));
+  c.row = reinterpret_cast<double*>(smem_raw + SPB);
   c.red = c.row + (size_t)P * c.S;
   c.bc = c.red + 64;
   c.scan = c.bc + 8;

@@ -362,6 +362,9 @@ struct mgb_step {
   bool vec16 = false;  // relax_win_kernel: 16-byte row accesses
   int threads = 32, smem = 0, max_grid = 1, sms = 148;
   const void* fn = nullptr;
+  // SL_GMRES single-CTA: 2 CTAs/SM variant for levels that need > 1 wave of fn
+  const void* fn2 = nullptr;
+  int smem2 = 0, max_grid2 = 0;
   double* ws = nullptr;
   long long ws_slot = 0;
   int ws_slots = 0;
@@ -703,6 +706,25 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   }
   st->max_grid = nb * sms;
   st->sms = sms;
+  if (dk == mgb::K_SLG && T <= 256 && nb == 1) {
+    static const bool no_occ2 = std::getenv("MGB_SLG_NO_OCC2") != nullptr;
+    const void* fn2 = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(reg_mutex());
+      auto it2 = registry().find(std::make_tuple((int)dk, P, span, 3, st->exact));
+      if (it2 != registry().end()) fn2 = it2->second;
+    }
+    const int smem2 = st->smem - (int)sizeof(StepParams) + mgb::sp_smem_bytes<mgb::K_SLG, 2>();
+    int nb2 = 0;
+    if (fn2 && !no_occ2 && raise_smem_attr(fn2, smem2) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, fn2, st->threads, smem2) == cudaSuccess &&
+        nb2 >= 2) {
+      st->fn2 = fn2;
+      st->smem2 = smem2;
+      st->max_grid2 = nb2 * sms;
+    }
+    cudaGetLastError();
+  }
   prepare_clusters(st);
   e = cudaMalloc(&st->dp, sizeof(StepParams));
   if (e != cudaSuccess) { delete st; return fail(MGB_ERR_CUDA, "cudaMalloc params"); }
@@ -736,7 +758,7 @@ int mgb_step_reserve_workspace(mgb_step* st, void* stream) {
   const long long cap = st->hp.cap, n = st->hp.n;
   st->ws_slot = (cap + 1) * n + cap * cap + 3 * cap + 1;
   st->ws_slot = (st->ws_slot + 31) / 32 * 32;
-  st->ws_slots = st->max_grid;
+  st->ws_slots = std::max(st->max_grid, st->fn2 ? st->max_grid2 : 0);
   CUDA_TRY(cudaMalloc(&st->ws, (size_t)st->ws_slot * st->ws_slots * sizeof(double)));
   return MGB_OK;
 }
@@ -838,6 +860,16 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
     if (rc) return rc;
     L.ws = st->ws;
     L.ws_slot = st->ws_slot;
+    if (st->fn2 && a->n_intervals > st->max_grid) {  // one wave at 2 CTAs/SM instead of two
+      const long long grid2 = std::min<long long>(std::min<long long>(a->n_intervals, st->max_grid2),
+                                                  st->ws_slots);
+      const StepParams* dp2 = st->dp;
+      void* args2[] = {(void*)&dp2, (void*)&L};
+      CUDA_TRY(cudaLaunchKernel(st->fn2, dim3((unsigned)grid2), dim3(st->threads), args2,
+                                (size_t)st->smem2, (cudaStream_t)stream));
+      g_launches++;
+      return MGB_OK;
+    }
     grid = std::min<long long>(grid, st->ws_slots);
   }
   const StepParams* dp = st->dp;
