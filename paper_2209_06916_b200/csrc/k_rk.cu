@@ -8,7 +8,13 @@ namespace mgb {
   MGB_REG(K_RK, P, 0, 3, true); \
   MGB_REG(K_RK, P, 0, 4, true); \
   MGB_REG(K_RK, P, 0, 5, true); \
-  MGB_REG(K_RK, P, 0, 6, true);
+  MGB_REG(K_RK, P, 0, 6, true); \
+  MGB_REG(K_RK, P, 0, 1 + RK_ZSOLVE, true); \
+  MGB_REG(K_RK, P, 0, 2 + RK_ZSOLVE, true); \
+  MGB_REG(K_RK, P, 0, 3 + RK_ZSOLVE, true); \
+  MGB_REG(K_RK, P, 0, 4 + RK_ZSOLVE, true); \
+  MGB_REG(K_RK, P, 0, 5 + RK_ZSOLVE, true); \
+  MGB_REG(K_RK, P, 0, 6 + RK_ZSOLVE, true);
 void register_rk() {
   RK_P(1)
   RK_P(2)

@@ -48,6 +48,7 @@ constexpr int MAX_CAP = 128;
 constexpr int MAX_WIN = 31;  // register-window stencils: span <= 30
 
 enum { K_WIN = 0, K_GEN = 1, K_RK = 2, K_SLD = 3, K_SLG = 4, K_SLGC = 5, K_SLGC1 = 6 };
+constexpr int RK_ZSOLVE = 8;  // K_RK NST flag: SDIRK stage values cL y = (y - rhs) / gamma
 
 // One periodic first/second-order recurrence factor of a factorised
 // circulant (see bandsolve in mgb_host.cu):
@@ -68,7 +69,8 @@ struct StepParams {
   int implicit, nfac, shift, cap;
   int ntap, ntap2, win_lo, win_span;
   int win2_lo, win2_span, win2_ok, win1_ok;  // contiguous stencils: GMRES operator / RK -cL
-  double gain_inv, tol;
+  int z_solve, zpad_;  // SDIRK: stage value cL y = (y - rhs) / gamma from the stage solve
+  double gain_inv, tol, inv_gamma;
   double A[MAX_ST * MAX_ST], b[MAX_ST];
   int tap_off[MAX_TAPS];
   double tap_w[MAX_TAPS];
@@ -863,12 +865,15 @@ __device__ __forceinline__ void step_once(Ctx& c, const double (&wd)[SPAN + 1], 
     stencil_gen<P, true>(c, sp.ntap, sp.tap_off, sp.tap_w, b);
     gmres_solve<P>(c, b, y, depth, gres);
   } else {  // K_RK: staged Runge-Kutta sweep, stepping.py:363-378
+    // NST = stages (+ RK_ZSOLVE: SDIRK stage values from the stage solves)
+    constexpr int NS = NST & (RK_ZSOLVE - 1);
+    constexpr bool ZS = NST >= RK_ZSOLVE;
     double x[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) x[q] = c.own ? c.row[q * c.S + c.t] : 0.0;
-    double z[NST][P];
+    double z[NS][P];
 #pragma unroll
-    for (int i = 0; i < NST; ++i) {
+    for (int i = 0; i < NS; ++i) {
       double rhs[P];
 #pragma unroll
       for (int q = 0; q < P; ++q) rhs[q] = x[q];
@@ -879,6 +884,18 @@ __device__ __forceinline__ void step_once(Ctx& c, const double (&wd)[SPAN + 1], 
 #pragma unroll
           for (int q = 0; q < P; ++q) rhs[q] = __dadd_rn(rhs[q], __dmul_rn(aij, z[j][q]));
         }
+      }
+      if constexpr (ZS) {
+        // M y = rhs with M = I - gamma cL  =>  cL y = (y - rhs) / gamma: the
+        // stage value without the stencil pass (and its row round trip)
+        double r0[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) r0[q] = rhs[q];
+        if (i > 0) __syncthreads();  // previous solve's carry buffers are free
+        chain_solve<P>(c, rhs);
+#pragma unroll
+        for (int q = 0; q < P; ++q) z[i][q] = __dmul_rn(__dsub_rn(rhs[q], r0[q]), sp.inv_gamma);
+        continue;
       }
       if (sp.implicit) chain_solve<P>(c, rhs);
       CL_TR_INIT
@@ -896,7 +913,7 @@ __device__ __forceinline__ void step_once(Ctx& c, const double (&wd)[SPAN + 1], 
 #pragma unroll
     for (int q = 0; q < P; ++q) y[q] = x[q];
 #pragma unroll
-    for (int i = 0; i < NST; ++i) {
+    for (int i = 0; i < NS; ++i) {
       const double bi = sp.b[i];
       if (bi != 0.0) {
 #pragma unroll

@@ -596,6 +596,14 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
       for (int j = 0; j < d->stages; ++j) hp.A[i * mgb::MAX_ST + j] = d->rk_a[i * d->stages + j];
     }
     hp.implicit = d->implicit ? 1 : 0;
+    if (hp.implicit) {  // SDIRK: constant nonzero diagonal -> stage values from the solves
+      static const bool stencil_stages = std::getenv("MGB_RK_STENCIL") != nullptr;
+      const double g = hp.A[0];
+      bool ok = g != 0.0 && !stencil_stages;
+      for (int i = 1; i < d->stages; ++i) ok = ok && hp.A[i * mgb::MAX_ST + i] == g;
+      hp.z_solve = ok ? 1 : 0;
+      hp.inv_gamma = ok ? 1.0 / g : 0.0;
+    }
     // register-window form of the -cL stencil (contiguous, span <= 6)
     bool inc = true;
     for (int k = 1; k < d->n_taps; ++k) inc = inc && off[k] > off[k - 1];
@@ -656,7 +664,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->span = span;
   const bool win_dedicated = dk == mgb::K_WIN && T <= 256 && span < 16 && n % 2 == 0;
   st->vec16 = win_dedicated;
-  st->nst = dk == mgb::K_RK ? hp.stages : 1;
+  st->nst = dk == mgb::K_RK ? hp.stages + (hp.z_solve ? mgb::RK_ZSOLVE : 0) : 1;
   st->exact = (dk == mgb::K_WIN || dk == mgb::K_GEN) ? hp.exact : 1;
   st->threads = ((T + 31) / 32) * 32;
   size_t dbl = (size_t)P * S + 64 + 8;
