@@ -424,7 +424,8 @@ __device__ void chain_solve(Ctx& c, double (&x)[P]) {
 #pragma unroll
       for (int qq = 0; qq < P; ++qq) {
         const int q = fwd ? qq : P - 1 - qq;
-        const double yv = fma(a2, s2, fma(a1, s1, x[q]));
+        // the y_{q-2} term first: one FMA latency per point on the carried chain
+        const double yv = fma(a1, s1, fma(a2, s2, x[q]));
         x[q] = yv;
         s2 = s1;
         s1 = yv;
@@ -449,17 +450,25 @@ __device__ void chain_solve(Ctx& c, double (&x)[P]) {
       __syncthreads();
       CL_TR(5)
       if (c.own) {
+        // Horner over k = K..1: c = M c + s_{tl-k}; compact runtime loop (an
+        // unrolled 16-way predicated loop stalls on instruction fetch), next
+        // chunk's end state loaded one iteration ahead
         const M2r M = ld_m2(F.M);
         const int K = F.win;
-#pragma unroll
-        for (int k = 16; k >= 1; --k) {
-          if (k <= K) {
-            int u = tl - k;
-            u += u < 0 ? T : 0;
-            mv2r(M, c1, c2);
-            c1 += wb[u];
-            c2 += wb[T + u];
+        int u = tl - K;
+        u += u < 0 ? T : 0;
+        double n1 = wb[u], n2 = wb[T + u];
+#pragma unroll 1
+        for (int k = K; k >= 1; --k) {
+          const double b1 = n1, b2 = n2;
+          if (k > 1) {
+            u = u + 1 == T ? 0 : u + 1;
+            n1 = wb[u];
+            n2 = wb[T + u];
           }
+          mv2r(M, c1, c2);
+          c1 += b1;
+          c2 += b2;
         }
       }
       CL_TR(7)
