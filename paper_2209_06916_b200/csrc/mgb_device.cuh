@@ -667,7 +667,12 @@ struct GmLayout {
 // layout); the vectors an Arnoldi step needs are streamed into two shared
 // memory stages with TMA bulk copies (cp.async.bulk + mbarrier) two ahead of
 // use, so MGS reads them at shared-memory latency.  R and the Givens state
-// stay in shared memory; the back substitution runs on one warp.
+// stay in shared memory; the back substitution runs on one warp.  A stage
+// keeps the vector it holds across Arnoldi steps (shallow solves -- depth <= 3,
+// the common case on many-interval levels -- stream V_0 and V_1 once per
+// solve, not once per step), and the async-proxy fence for a new basis vector
+// is issued one step after its store (its first TMA read is two steps later),
+// so the stores drain off the critical path.
 template <int P>
 __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& depth_out,
                             double& res_out) {
@@ -687,15 +692,26 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   double* stage0 = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(c.gm + GmLayout::stage()) + 15) & ~uintptr_t(15));
   const uint32_t vbytes = (uint32_t)n * 8u;
+  // held[st]: basis index stage st holds (or will hold once its pending copy
+  // lands); pend: stages with a copy in flight.  Uniform across the CTA.
+  int held0 = -1, held1 = -1;
+  unsigned pend = 0;
 #define MGB_ISSUE(i, st)                                                      \
   do {                                                                        \
-    mbar_arm(bar + (st), vbytes);                                             \
-    bulk_g2s(stage0 + (size_t)(st) * n, V + (size_t)(i) * n, vbytes, bar + (st)); \
+    if (t == 0) {                                                             \
+      mbar_arm(bar + (st), vbytes);                                           \
+      bulk_g2s(stage0 + (size_t)(st) * n, V + (size_t)(i) * n, vbytes, bar + (st)); \
+    }                                                                         \
+    if (st) held1 = (i); else held0 = (i);                                    \
+    pend |= 1u << (st);                                                       \
   } while (0)
 #define MGB_CONSUME(st, vi)                                                   \
   do {                                                                        \
-    mbar_wait(bar + (st), (c.phase >> (st)) & 1u);                            \
-    c.phase ^= 1u << (st);                                                    \
+    if (pend & (1u << (st))) {                                                \
+      mbar_wait(bar + (st), (c.phase >> (st)) & 1u);                          \
+      c.phase ^= 1u << (st);                                                  \
+      pend &= ~(1u << (st));                                                  \
+    }                                                                         \
     if (c.own) vec_load<P>(stage0 + (size_t)(st) * n, t, T, vi);              \
   } while (0)
   CL_TR_INIT
@@ -717,8 +733,7 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   const double ib = 1.0 / beta;
 #pragma unroll
   for (int q = 0; q < P; ++q) v[q] = b[q] * ib;
-  if (c.own) vec_store<P>(V, t, T, v);
-  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> TMA reads
+  if (c.own) vec_store<P>(V, t, T, v);  // fenced for the TMA after step 0's stencil
   if (t == 0) gg[0] = beta;
   double res = 1.0;
   int depth = 0;
@@ -726,21 +741,26 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
     __syncthreads();
     if (c.own) chunk_to_row<P>(c.row, t, c.S, v);
     __syncthreads();
-    if (t == 0) {  // stream V_0, V_1 while the stencil runs (V_j itself is the row)
-      if (j >= 1) MGB_ISSUE(0, 0);
-      if (j >= 2) MGB_ISSUE(1, 1);
-    }
+    // stream V_0, V_1 while the stencil runs (V_j itself is the row), unless
+    // the stages still hold them
+    if (j >= 1 && held0 != 0) MGB_ISSUE(0, 0);
+    if (j >= 2 && held1 != 1) MGB_ISSUE(1, 1);
     CL_TR(9)
     double w[P];
     apply_op2<P>(c, w);
+    // generic stores of V_j (previous step / solve start) -> async-proxy reads;
+    // the first TMA read of V_j is issued after a later CTA barrier
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     CL_TR(1)
     for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
       double vi[P];
       if (i < j) {
         MGB_CONSUME(i & 1, vi);
-      } else {
+      } else {  // V_j is the row; idle threads (!c.own) read thread 0's slot,
+                // and every use of their values below is guarded by c.own
+        const double* rp = c.row + (c.own ? t : 0);
 #pragma unroll
-        for (int q = 0; q < P; ++q) vi[q] = c.own ? c.row[q * c.S + t] : 0.0;
+        for (int q = 0; q < P; ++q) vi[q] = rp[q * c.S];
       }
       double p0 = 0.0, p1 = 0.0;
       if (c.own) {
@@ -753,10 +773,8 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
       CL_TR(2)
       const double h = block_sum(c, p0 + p1);  // every thread has consumed stage i&1
       CL_TR(3)
-      if (t == 0) {
-        hcol[i] = h;
-        if (i + 2 < j) MGB_ISSUE(i + 2, i & 1);
-      }
+      if (t == 0) hcol[i] = h;
+      if (i + 2 < j) MGB_ISSUE(i + 2, i & 1);
 #pragma unroll
       for (int q = 0; q < P; ++q) w[q] = fma(-h, vi[q], w[q]);
     }
@@ -775,8 +793,7 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
     const double inv = 1.0 / (hn > 0.0 ? hn : 1.0);
 #pragma unroll
     for (int q = 0; q < P; ++q) v[q] = w[q] * inv;
-    if (c.own) vec_store<P>(V + (size_t)(j + 1) * n, t, T, v);
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (c.own) vec_store<P>(V + (size_t)(j + 1) * n, t, T, v);  // fenced next step
     if (t == 0) {  // Givens (circulant.py:308-319), rotated entry carried in a register
       double hi = hcol[0];
 #pragma unroll 4
