@@ -849,7 +849,25 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < P; ++q) x[q] = 0.0;
-  if (c.own) {  // x = V y: basis streamed from L2 with a two-deep register prefetch
+  if (c.own && depth <= 3) {  // x = V y from shared memory: V_{depth-1} is the
+    // row, V_0 / V_1 are still in the stages (every copy has been consumed)
+    for (int i = 0; i < depth; ++i) {
+      const double yi = ybuf[i];
+      double vi[P];
+      if (i == depth - 1) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) vi[q] = c.row[q * c.S + t];
+      } else if (i == held0) {
+        vec_load<P>(stage0, t, T, vi);
+      } else if (i == held1) {
+        vec_load<P>(stage0 + n, t, T, vi);
+      } else {
+        vec_load<P>(V + (size_t)i * n, t, T, vi);
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q) x[q] = fma(yi, vi[q], x[q]);
+    }
+  } else if (c.own) {  // x = V y: basis streamed from L2 with a two-deep register prefetch
     double va[P], vb[P];
     vec_load<P>(V, t, T, va);
     if (depth > 1) vec_load<P>(V + n, t, T, vb);
