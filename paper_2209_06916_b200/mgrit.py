@@ -23,6 +23,7 @@ bitwise on the reference).
 
 from __future__ import annotations
 
+import ctypes
 import math
 import time
 from dataclasses import dataclass
@@ -273,6 +274,7 @@ class MgritSolver:
         n0 = self.levels[0].n_int
         self.partials = torch.empty(max(n0, 1), dtype=torch.float64, device="cuda")
         self.sumbuf = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self.sumbuf0 = torch.zeros(1, dtype=torch.float64, device="cuda")
         self._built = True
 
     # ---------------------------------------------------------- iteration
@@ -309,7 +311,7 @@ class MgritSolver:
         return out
 
     def _cycle(self, l: int, u: int, g: Optional[int], u_zero: bool, want_norm: bool,
-               kind: Optional[str] = None) -> None:
+               kind: Optional[str] = None, pre_cf=None) -> None:
         cfg = self.config
         kind = kind or cfg.cycle
         L = self.levels[l]
@@ -334,6 +336,8 @@ class MgritSolver:
                     c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
                     tail_out=ptr(gC) + row, tail_stride=n, g=g)
         self._coarse_solve(l + 1, kind)
+        if pre_cf is not None:  # last reader of the incoming F-points (solve's initial norm)
+            pre_cf()
         fuse_norm = want_norm and cfg.nu > 0
         if cfg.nu == 0:
             c_src, c_stride = (None if u_zero else u), m * n
@@ -374,10 +378,21 @@ class MgritSolver:
         L.plan.relax(L.n_int, m, 0, c_src=u + (m - 1) * n * _F64, c_stride=m * n, tail=2,
                      cref=u + m * n * _F64, cref_stride=m * n, g=g, partials=ptr(self.partials))
 
-    def _norm(self) -> float:
+    def _norm(self, buf=None) -> float:
+        buf = self.sumbuf if buf is None else buf
+        self._timed("norm", device_sum, ptr(self.partials), self.levels[0].n_int, ptr(buf))
+        return math.sqrt(float(buf.item()))
+
+    def _initial_norm_deferred(self, ev):
+        """pre_cf hook of the first cycle when the rows before the C-points are
+        still in flight (``_upload(split=True)``): wait for them, then the
+        initial residual partials and their sum into ``sumbuf0`` -- before the
+        CF pass rewrites the F-points and reuses the partials buffer."""
+        torch = self._torch
+        torch.cuda.current_stream().wait_event(ev)
+        self._timed("L0.R", self._residual_partials, ptr(self._u_dev), None)
         self._timed("norm", device_sum, ptr(self.partials), self.levels[0].n_int,
-                    ptr(self.sumbuf))
-        return math.sqrt(float(self.sumbuf.item()))
+                    ptr(self.sumbuf0))
 
     def iterate(self, u, g=None):
         """One MGRIT cycle in place; returns the updated iterate (mgrit.py:218-223)."""
@@ -401,17 +416,32 @@ class MgritSolver:
         internal = u is None
         if internal:
             u = self.initial_state()
-        ud, uh = self._upload(u)
+        ud, uh, pending = self._upload(u, split=True)
         up = ptr(ud)
-        torch.cuda.synchronize()
-        start = time.perf_counter()
-        self._timed("L0.R", self._residual_partials, up, None)
-        norms = [self._norm()]
+        hook = None
+        if pending is None:
+            torch.cuda.synchronize()
+            start = time.perf_counter()
+            self._timed("L0.R", self._residual_partials, up, None)
+            norms = [self._norm()]
+        else:
+            # the C-points have landed; the rows before them are still in
+            # flight on the copy stream and are first read by the initial
+            # residual, which runs inside the first cycle before its CF pass
+            torch.cuda.current_stream().synchronize()
+            start = time.perf_counter()
+            self._u_dev = ud
+            hook = lambda: self._initial_norm_deferred(pending)  # noqa: E731
+            norms = []
         converged = False
         it = 0
         while it < cfg.max_iters:
-            self._cycle(0, up, None, False, True)
+            self._cycle(0, up, None, False, True, pre_cf=hook)
             it += 1
+            if hook is not None:
+                hook = None
+                self._u_dev = None
+                norms.append(math.sqrt(float(self.sumbuf0.item())))
             norms.append(self._norm())
             if norms[0] > 0 and norms[-1] / norms[0] <= cfg.tol:
                 converged = True
@@ -424,7 +454,7 @@ class MgritSolver:
         rho = norms[-1] / norms[-2] if len(norms) >= 2 and norms[-2] > 0 else 0.0
         return SolveReport(norms, it, float(rho), converged, wall)
 
-    def _upload(self, u):
+    def _upload(self, u, split: bool = False):
         """Device copy of a host iterate for ``solve``: only the rows the solve
         reads before rewriting them -- the C-points u[km] and the rows
         u[km-1] before them (initial residual, mgrit.py:164-166 / 259-261; the
@@ -433,16 +463,23 @@ class MgritSolver:
         every F-point before any is read, so the other rows of the initial
         iterate cannot influence the result (tests/test_gpu_parity.py checks
         host and device inputs give bitwise identical solves, with the
-        skipped rows poisoned).  CUDA tensors are used in place."""
+        skipped rows poisoned).  CUDA tensors are used in place.
+
+        Returns ``(device iterate, caller's array, pending)``.  With ``split``
+        and a pinned host tensor the rows before the C-points travel on a
+        side copy stream and ``pending`` is the CUDA event that marks their
+        arrival (the caller makes its stream wait on it before the first
+        read); otherwise ``pending`` is None and both copies are ordered on
+        the current stream."""
         torch = self._torch
         pr = self.problem
         m = pr.m[0] if pr.m else 0
         self.last_upload_bytes = 0
         if is_tensor(u) and u.is_cuda:
-            return to_device(u)
+            return to_device(u) + (None,)
         if m < 3:
             self.last_upload_bytes = 8 * (pr.n_t + 1) * pr.n_x
-            return to_device(u)
+            return to_device(u) + (None,)
         shape = (pr.n_t + 1, pr.n_x)
         if is_tensor(u):
             if u.dtype != torch.float64:
@@ -460,13 +497,26 @@ class MgritSolver:
         n_int = pr.n_t // m
         h, d = src.data_ptr(), ud.data_ptr()
         lib, stream = nat_load(), stream_handle()
+        pinned = is_tensor(u) and u.is_pinned()
+        pending = None
         nat_check(lib.mgb_copy_rows(d, m * row, h, m * row, row, n_int + 1, stream))
-        nat_check(lib.mgb_copy_rows(d + (m - 1) * row, m * row, h + (m - 1) * row, m * row, row,
-                                    n_int, stream))
+        if split and pinned:
+            cur = torch.cuda.current_stream()
+            side = getattr(self, "_copy_stream", None)
+            if side is None:
+                side = self._copy_stream = torch.cuda.Stream()
+            side.wait_stream(cur)  # ud's allocation / poison fill come first
+            nat_check(lib.mgb_copy_rows(d + (m - 1) * row, m * row, h + (m - 1) * row, m * row,
+                                        row, n_int, ctypes.c_void_p(side.cuda_stream)))
+            pending = torch.cuda.Event()
+            pending.record(side)
+        else:
+            nat_check(lib.mgb_copy_rows(d + (m - 1) * row, m * row, h + (m - 1) * row, m * row,
+                                        row, n_int, stream))
         self.last_upload_bytes = (2 * n_int + 1) * row
-        if not (is_tensor(u) and u.is_pinned()):
+        if not pinned:
             torch.cuda.current_stream().synchronize()  # pageable source: keep it alive
-        return ud, u
+        return ud, u, pending
 
 
 def solve(problem: TimeGridProblem, config: MgritConfig, threads: int = 1,

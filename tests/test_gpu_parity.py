@@ -357,3 +357,24 @@ def test_host_iterate_upload_of_live_rows_only(fam, p, c, n_x, n_t, m, cyc, monk
     assert not np.isnan(ref).any()
     # default solve (internal iterate) gives the same history
     assert P.solve(prob, cfg).residual_norms == r_dev.residual_norms
+
+
+@pytest.mark.parametrize("nu", [0, 2])
+def test_pinned_upload_overlap_any_nu(nu, monkeypatch):
+    """The pinned-host solve overlaps the upload of the rows before the
+    C-points with the first cycle (the initial residual runs just before the
+    first CF pass); for every relaxation count it equals the device-iterate
+    solve bitwise, with the skipped rows poisoned."""
+    import torch
+    from paper_2209_06916_b200 import mgrit as M
+    monkeypatch.setattr(M, "POISON_SKIPPED_ROWS", True)
+    prob = P.experiments.build_problem(P.DiscretizationSpec("erk", 3, 0.85, 256, 1024), 8,
+                                       "v_cycle", "modified")
+    cfg = P.MgritConfig(cycle="v_cycle", nu=nu)
+    u0 = P.MgritSolver(prob, cfg).initial_state()
+    dev = torch.from_numpy(u0.copy()).cuda()
+    r_dev = P.solve(prob, cfg, initial_iterate=dev)
+    host_t = torch.from_numpy(u0.copy()).pin_memory()
+    r_t = P.solve(prob, cfg, initial_iterate=host_t)
+    assert r_t.residual_norms == r_dev.residual_norms and r_t.iterations == r_dev.iterations
+    assert np.array_equal(host_t.numpy(), dev.cpu().numpy())

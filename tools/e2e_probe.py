@@ -40,7 +40,7 @@ def main(cfg_name="cfg2", reps=4):
         s._build()
         torch.cuda.synchronize()
         t.append(time.perf_counter())
-        ud, uh = s._upload(host)
+        ud, uh, _ = s._upload(host)
         torch.cuda.synchronize()
         t.append(time.perf_counter())
         rep = s.solve(ud)
