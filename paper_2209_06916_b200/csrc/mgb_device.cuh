@@ -194,10 +194,19 @@ __device__ __forceinline__ double block_sum(Ctx& c, double v) {
   if (lane == 0) slot[w] = v;
   __syncthreads();
   const int nw = blockDim.x >> 5;
-  double s = lane < nw ? slot[lane] : 0.0;
-  for (int o = 16; o > 0; o >>= 1)
-    if (o < nw) s += __shfl_xor_sync(0xffffffffu, s, o);  // lanes >= nw hold 0
-  s = __shfl_sync(0xffffffffu, s, 0);
+  double s;
+  if (nw == 8) {  // broadcast reads in lane 0's butterfly order (bitwise the same
+                  // sum as the generic path below, without its shuffle chain)
+    s = ((slot[0] + slot[4]) + (slot[2] + slot[6])) + ((slot[1] + slot[5]) + (slot[3] + slot[7]));
+  } else if (nw == 16) {
+    s = (((slot[0] + slot[8]) + (slot[4] + slot[12])) + ((slot[2] + slot[10]) + (slot[6] + slot[14]))) +
+        (((slot[1] + slot[9]) + (slot[5] + slot[13])) + ((slot[3] + slot[11]) + (slot[7] + slot[15])));
+  } else {
+    s = lane < nw ? slot[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1)
+      if (o < nw) s += __shfl_xor_sync(0xffffffffu, s, o);  // lanes >= nw hold 0
+    s = __shfl_sync(0xffffffffu, s, 0);
+  }
   c.parity ^= 1;
   return s;
 }
