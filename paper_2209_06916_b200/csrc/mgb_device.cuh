@@ -695,11 +695,25 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   double* cs = c.gm + GmLayout::cs();
   double* sn = c.gm + GmLayout::sn();
   double* gg = c.gm + GmLayout::gg();
-  double* R = cap <= RS_CAP ? c.gm + GmLayout::Rs() : Rg;
-  const int ldr = cap <= RS_CAP ? RS_CAP : cap;
+  // R in shared memory for cap <= RS_CAP, else in the global slot; accessed
+  // through a uniform branch so the shared case compiles to LDS/STS (one
+  // pointer selected between the two spaces would be generic)
+  double* const Rs = c.gm + GmLayout::Rs();
+  const bool rsm = cap <= RS_CAP;
+  const int ldr = rsm ? RS_CAP : cap;
+  auto rget = [&](int col, int r) -> double {
+    const size_t k = (size_t)col * ldr + r;
+    return rsm ? Rs[k] : Rg[k];
+  };
+  auto rset = [&](int col, int r, double v) {
+    const size_t k = (size_t)col * ldr + r;
+    if (rsm) Rs[k] = v; else Rg[k] = v;
+  };
   uint64_t* bar = reinterpret_cast<uint64_t*>(c.gm + GmLayout::mbar());
-  double* stage0 = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(c.gm + GmLayout::stage()) + 15) & ~uintptr_t(15));
+  // 16-byte aligned stage base by pointer arithmetic on the shared pointer (an
+  // integer round trip would lose the address space: generic LD.E instead of LDS)
+  double* stage0 = c.gm + GmLayout::stage();
+  stage0 += ((uint32_t)__cvta_generic_to_shared(stage0) & 15u) ? 1 : 0;
   const uint32_t vbytes = (uint32_t)n * 8u;
   // held[st]: basis index stage st holds (or will hold once its pending copy
   // lands); pend: stages with a copy in flight.  Uniform across the CTA.
@@ -808,7 +822,7 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
 #pragma unroll 4
       for (int i = 0; i < j; ++i) {
         const double ci = cs[i], si = sn[i], hi1 = hcol[i + 1];
-        R[(size_t)j * ldr + i] = __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1));
+        rset(j, i, __dadd_rn(__dmul_rn(ci, hi), __dmul_rn(si, hi1)));
         hi = __dadd_rn(__dmul_rn(-si, hi), __dmul_rn(ci, hi1));
       }
       double den = hypot(hi, hn);
@@ -817,7 +831,7 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
       const double cj = hi * rd, sj = hn * rd;
       cs[j] = cj;
       sn[j] = sj;
-      R[(size_t)j * ldr + j] = __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn));
+      rset(j, j, __dadd_rn(__dmul_rn(cj, hi), __dmul_rn(sj, hn)));
       const double gj = gg[j];
       gg[j + 1] = __dmul_rn(-sj, gj);
       gg[j] = __dmul_rn(cj, gj);
@@ -839,18 +853,18 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
       double y = lane < depth ? gg[lane] : 0.0;
       for (int jj = depth - 1; jj >= 0; --jj) {
         double yj = __shfl_sync(0xffffffffu, y, jj);
-        if (yj != 0.0) yj /= R[(size_t)jj * ldr + jj];
+        if (yj != 0.0) yj /= rget(jj, jj);
         if (lane == jj) y = yj;
-        if (lane < jj) y = __dsub_rn(y, __dmul_rn(yj, R[(size_t)jj * ldr + lane]));
+        if (lane < jj) y = __dsub_rn(y, __dmul_rn(yj, rget(jj, lane)));
       }
       if (lane < depth) ybuf[lane] = y;
     } else if (lane == 0) {
       for (int i = 0; i < depth; ++i) ybuf[i] = gg[i];
       for (int jj = depth - 1; jj >= 0; --jj) {
         if (ybuf[jj] != 0.0) {
-          ybuf[jj] /= R[(size_t)jj * ldr + jj];
+          ybuf[jj] /= rget(jj, jj);
           const double yj = ybuf[jj];
-          for (int i = 0; i < jj; ++i) ybuf[i] = __dsub_rn(ybuf[i], __dmul_rn(yj, R[(size_t)jj * ldr + i]));
+          for (int i = 0; i < jj; ++i) ybuf[i] = __dsub_rn(ybuf[i], __dmul_rn(yj, rget(jj, i)));
         }
       }
     }
