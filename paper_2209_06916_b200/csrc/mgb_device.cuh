@@ -654,6 +654,60 @@ __device__ __forceinline__ void apply_op2(const Ctx& c, double (&y)[P]) {
   stencil_win_rt<P, false>(c, sp.win2_lo, sp.win2_span, sp.win2_w, y);
 }
 
+// (I - phi D) on a basis vector held in registers (P consecutive points per
+// thread), symmetric window -R..R: neighbour points come from the adjacent
+// lanes by shuffles, across warp boundaries from the per-warp edge slots
+// (e[0..2] = lane 0's first three points, e[4..6] = lane 31's last three,
+// written before the CTA barrier that precedes this call).  Same taps and
+// accumulation order as stencil_win_rt (bitwise the same y), without the
+// row round trip through shared memory and its two CTA barriers.
+template <int P, int R>
+__device__ __forceinline__ void stencil_shfl(const Ctx& c, const double* wts, const double (&v)[P],
+                                             const double* edges, double (&y)[P]) {
+  const int lane = c.t & 31, wp = c.t >> 5, nw = c.T >> 5;
+  double win[P + 2 * R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    win[r] = __shfl_up_sync(0xffffffffu, v[P - R + r], 1);
+    win[P + R + r] = __shfl_down_sync(0xffffffffu, v[r], 1);
+  }
+  if (lane == 0) {
+    const double* e = edges + 8 * (wp == 0 ? nw - 1 : wp - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) win[r] = e[4 + 3 - R + r];
+  }
+  if (lane == 31) {
+    const double* e = edges + 8 * (wp == nw - 1 ? 0 : wp + 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) win[P + R + r] = e[r];
+  }
+#pragma unroll
+  for (int q = 0; q < P; ++q) win[R + q] = v[q];
+#pragma unroll
+  for (int q = 0; q < P; ++q) y[q] = 0.0;
+#pragma unroll
+  for (int k = 0; k <= 2 * R; ++k) {
+    const double wk = wts[k];
+#pragma unroll
+    for (int q = 0; q < P; ++q) y[q] = madd<false>(y[q], wk, win[q + k]);
+  }
+}
+
+// edge slots of this thread's basis chunk for stencil_shfl (lanes 0 and 31)
+template <int P>
+__device__ __forceinline__ void put_edges(const Ctx& c, const double (&v)[P], double* edges) {
+  const int lane = c.t & 31;
+  double* e = edges + 8 * (c.t >> 5);
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) e[r] = v[r < P ? r : 0];
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) e[4 + r] = v[P - 3 + r >= 0 ? P - 3 + r : 0];
+  }
+}
+
 constexpr int RS_CAP = 24;  // Hessenberg R kept in shared memory for cap <= RS_CAP
 
 // Shared-memory carve-up of the single-CTA GMRES (after the scan area), doubles
@@ -665,7 +719,8 @@ struct GmLayout {
   __host__ __device__ static int gg() { return sn() + MAX_CAP; }
   __host__ __device__ static int Rs() { return gg() + MAX_CAP + 2; }
   __host__ __device__ static int mbar() { return Rs() + RS_CAP * RS_CAP; }
-  __host__ __device__ static int stage() { return mbar() + 4; }  // + 16-byte alignment pad
+  __host__ __device__ static int edges() { return mbar() + 4; }  // 8 doubles per warp (<= 16 warps)
+  __host__ __device__ static int stage() { return edges() + 8 * 16; }  // + 16-byte alignment pad
   __host__ __device__ static int total(int n) { return stage() + 2 + 2 * n; }
 };
 
@@ -758,19 +813,39 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   for (int q = 0; q < P; ++q) v[q] = b[q] * ib;
   if (c.own) vec_store<P>(V, t, T, v);  // fenced for the TMA after step 0's stencil
   if (t == 0) gg[0] = beta;
+  // register/shuffle stencil path: symmetric contiguous operator window of
+  // half-width 1..3, every thread owning a chunk, whole warps (uniform)
+  double* const edges = c.gm + GmLayout::edges();
+  const int rh = sp.win2_span / 2;
+  const bool shfl = P >= 4 && sp.win2_ok && (sp.win2_span & 1) == 0 && rh >= 1 && rh <= 3 &&
+                    sp.win2_lo == n - rh && T == (int)blockDim.x && (T & 31) == 0 && T <= 512;
+  if (shfl) {
+    put_edges<P>(c, v, edges);
+    __syncthreads();
+  }
   double res = 1.0;
   int depth = 0;
   for (int j = 0; j < cap; ++j) {
-    __syncthreads();
-    if (c.own) chunk_to_row<P>(c.row, t, c.S, v);
-    __syncthreads();
+    if (shfl) {  // own slots only: V_j for the MGS i == j term and x = V y
+      chunk_to_row<P>(c.row, t, c.S, v);
+    } else {
+      __syncthreads();
+      if (c.own) chunk_to_row<P>(c.row, t, c.S, v);
+      __syncthreads();
+    }
     // stream V_0, V_1 while the stencil runs (V_j itself is the row), unless
     // the stages still hold them
     if (j >= 1 && held0 != 0) MGB_ISSUE(0, 0);
     if (j >= 2 && held1 != 1) MGB_ISSUE(1, 1);
     CL_TR(9)
     double w[P];
-    apply_op2<P>(c, w);
+    if (shfl) {
+      if (rh == 2) stencil_shfl<P, 2>(c, sp.win2_w, v, edges, w);
+      else if (rh == 3) stencil_shfl<P, 3>(c, sp.win2_w, v, edges, w);
+      else stencil_shfl<P, 1>(c, sp.win2_w, v, edges, w);
+    } else {
+      apply_op2<P>(c, w);
+    }
     // generic stores of V_j (previous step / solve start) -> async-proxy reads;
     // the first TMA read of V_j is issued after a later CTA barrier
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -817,6 +892,7 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
 #pragma unroll
     for (int q = 0; q < P; ++q) v[q] = w[q] * inv;
     if (c.own) vec_store<P>(V + (size_t)(j + 1) * n, t, T, v);  // fenced next step
+    if (shfl) put_edges<P>(c, v, edges);  // read after the barrier below
     if (t == 0) {  // Givens (circulant.py:308-319), rotated entry carried in a register
       double hi = hcol[0];
 #pragma unroll 4
