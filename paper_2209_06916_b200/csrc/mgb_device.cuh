@@ -948,9 +948,26 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < P; ++q) x[q] = 0.0;
-  if (c.own && depth <= 3) {  // x = V y from shared memory: V_{depth-1} is the
-    // row, V_0 / V_1 are still in the stages (every copy has been consumed)
-    for (int i = 0; i < depth; ++i) {
+  if (c.own) {  // x = V y, in basis order.  The last three vectors are on chip:
+    // V_{depth-1} is the row, V_{depth-2} / V_{depth-3} are in the stages (every
+    // copy has been consumed); the older ones stream from L2 with a two-deep
+    // register prefetch.
+    const int ng = depth > 3 ? depth - 3 : 0;
+    if (ng > 0) {
+      double va[P], vb[P];
+      vec_load<P>(V, t, T, va);
+      if (ng > 1) vec_load<P>(V + n, t, T, vb);
+      for (int i = 0; i < ng; ++i) {
+        const double yi = ybuf[i];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          x[q] = fma(yi, va[q], x[q]);
+          va[q] = vb[q];
+        }
+        if (i + 2 < ng) vec_load<P>(V + (size_t)(i + 2) * n, t, T, vb);
+      }
+    }
+    for (int i = ng; i < depth; ++i) {
       const double yi = ybuf[i];
       double vi[P];
       if (i == depth - 1) {
@@ -965,19 +982,6 @@ __device__ void gmres_solve(Ctx& c, const double (&b)[P], double (&x)[P], int& d
       }
 #pragma unroll
       for (int q = 0; q < P; ++q) x[q] = fma(yi, vi[q], x[q]);
-    }
-  } else if (c.own) {  // x = V y: basis streamed from L2 with a two-deep register prefetch
-    double va[P], vb[P];
-    vec_load<P>(V, t, T, va);
-    if (depth > 1) vec_load<P>(V + n, t, T, vb);
-    for (int i = 0; i < depth; ++i) {
-      const double yi = ybuf[i];
-#pragma unroll
-      for (int q = 0; q < P; ++q) {
-        x[q] = fma(yi, va[q], x[q]);
-        va[q] = vb[q];
-      }
-      if (i + 2 < depth) vec_load<P>(V + (size_t)(i + 2) * n, t, T, vb);
     }
   }
 #undef MGB_ISSUE
