@@ -1165,6 +1165,11 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __r
     const int nsteps = a.n_fsteps + (a.tail ? 1 : 0);
     for (int j = 1; j <= nsteps; ++j) {
       const bool is_tail = j > a.n_fsteps;
+      if (a.g && c.own) {  // this step's rhs chunk into L1 while the step runs (one line per
+                           // thread at P = 16): its load after the step no longer waits on L2
+        const double* gp1 = a.g + (is_tail ? rowbase + a.m : rowbase + j) * n + (size_t)t * P;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(gp1));
+      }
       for (int r = 0; r < reps; ++r) {
         step_once<P, KIND, SPAN, NST, EXACT>(c, wd, tb, r0, y, depth, gres);
         if (r + 1 < reps) {
