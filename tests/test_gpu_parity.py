@@ -378,3 +378,40 @@ def test_pinned_upload_overlap_any_nu(nu, monkeypatch):
     r_t = P.solve(prob, cfg, initial_iterate=host_t)
     assert r_t.residual_norms == r_dev.residual_norms and r_t.iterations == r_dev.iterations
     assert np.array_equal(host_t.numpy(), dev.cpu().numpy())
+
+
+_SINGLE_CTA_CHECK = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2209_06916_b200 as P
+from oracle import mgrit_oracle as O
+worst = 0.0
+for p, c, n, m, cum in [(1, 0.6, 1024, 4, 16), (3, 0.85, 1024, 8, 64), (5, 0.85, 1024, 16, 256),
+                        (3, 0.85, 4096, 8, 64), (5, 0.85, 4096, 16, 256)]:
+    cap = 10 if p == 1 else 20
+    spec = P.DiscretizationSpec("erk", p, c, n, 64)
+    st = P.modified_coarse_stepper(spec, m, 1, solver="gmres", gmres_max_iters=cap,
+                                   cumulative_factor=cum)
+    ost = O.corrected_coarse("erk", p, c, n, m, 1, "gmres", cap=cap, cumulative=cum)
+    v = np.random.default_rng(7).random((12, n))
+    ref, out = ost.apply(v), st.apply(v)
+    err = np.max(np.abs(out - ref)) / np.max(np.abs(ref))
+    assert err <= 1e-11, (p, n, err)
+    worst = max(worst, err)
+print("ok", worst)
+"""
+
+
+@pytest.mark.parametrize("extra_env", [{}, {"MGB_SLG_NO_OCC2": "1"}])
+def test_single_cta_gmres_every_stencil_width(extra_env):
+    """The single-CTA GMRES kernel (forced with MGB_NO_CLUSTER; the default
+    picks it for levels with many intervals) against the oracle for operator
+    half-widths 1, 2, 3 (p = 1, 3, 5) at 4 and 16 points per thread -- the
+    register/shuffle stencil path -- in both occupancy builds."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MGB_NO_CLUSTER="1", **extra_env)
+    r = subprocess.run([sys.executable, "-c", _SINGLE_CTA_CHECK.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
