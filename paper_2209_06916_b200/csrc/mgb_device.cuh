@@ -1089,12 +1089,18 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __r
                                                            const RelaxLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int SPB = sp_smem_bytes<KIND, MINB>();
+#ifdef MGB_CL_TRACE
+  const long long kt0_ = clock64();
+#endif
   {
     const int4* src = reinterpret_cast<const int4*>(gp);
     int4* dst = reinterpret_cast<int4*>(smem_raw);
     for (int i = threadIdx.x; i < SPB / 16; i += blockDim.x) dst[i] = src[i];
   }
   __syncthreads();
+#ifdef MGB_CL_TRACE  // slot 10: parameter prologue, slot 11: whole kernel (block 0)
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_cl_trace[10], (unsigned long long)(clock64() - kt0_));
+#endif
   const StepParams& sp = *reinterpret_cast<const StepParams*>(smem_raw);
   const mgb_relax_args& a = L.a;
   Ctx c;
@@ -1257,6 +1263,9 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __r
       if (a.stats_res) a.stats_res[k] = gres;
     }
   }
+#ifdef MGB_CL_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_cl_trace[11], (unsigned long long)(clock64() - kt0_));
+#endif
 }
 
 // ------------------------------------------- explicit-stencil relaxation
