@@ -1343,7 +1343,19 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
   const mgb_relax_args& a = L.a;
   const int nthr = blockDim.x;
   const uint32_t rowbytes = (uint32_t)n * 8u;
-  for (long long k = blockIdx.x; k < a.n_intervals; k += gridDim.x) {
+  // Contiguous interval blocks per CTA.  When the residual tail of interval k
+  // reads exactly the rows the head of interval k+1 starts from (CF and FR
+  // passes: cref = c_src + c_stride, cref_e = e + e_stride), the tail leaves the
+  // corrected C-point C_{k+1} (+ e_{k+1}) in the free slice buffer and writes
+  // c_out, so the next head needs no global loads (the same __dadd_rn sum).
+  const long long nI = a.n_intervals, G = gridDim.x;
+  const long long kb0 = (long long)blockIdx.x * nI / G, kb1 = ((long long)blockIdx.x + 1) * nI / G;
+  const bool chain = a.tail == 2 && a.c_src && a.cref == a.c_src + a.c_stride &&
+                     a.cref_stride == a.c_stride &&
+                     ((!a.e && !a.cref_e) ||
+                      (a.e && a.cref_e == a.e + a.e_stride && a.cref_e_stride == a.e_stride));
+  int have = -1;  // slice buffer already holding this interval's start row
+  for (long long k = kb0; k < kb1; ++k) {
     const long long kg = a.k_global0 + k;
     const long long rowbase = k * (long long)a.m;
     const double* csrc = (kg == 0 && a.c_src0) ? a.c_src0 : (a.c_src ? a.c_src + k * a.c_stride : nullptr);
@@ -1351,7 +1363,8 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
     __syncthreads();  // previous interval's readers of both buffers are done
     // interval start: C-point (+ correction, mgrit.py:246) -> slice buffer 0 (and c_out)
     // loads batched WIN_U deep (all in flight before the first use)
-    for (int i0 = 2 * t; i0 < n; i0 += 2 * nthr * WIN_U) {
+    const int start_buf = have >= 0 ? have : 0;
+    for (int i0 = 2 * t; have < 0 && i0 < n; i0 += 2 * nthr * WIN_U) {
       double2 y[WIN_U], ev[WIN_U];
 #pragma unroll
       for (int u = 0; u < WIN_U; ++u) {
@@ -1373,9 +1386,10 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
         }
       }
     }
+    have = -1;
     if (t == 0) {  // warm L2 for the next interval this CTA handles
-      const long long kn = k + gridDim.x;
-      if (kn < a.n_intervals) {
+      const long long kn = k + 1;
+      if (kn < kb1) {
         if (a.c_src) l2_prefetch(a.c_src + kn * a.c_stride, rowbytes);
         if (a.e) l2_prefetch(a.e + kn * a.e_stride, rowbytes);
         if (a.tail == 2 && a.cref) l2_prefetch(a.cref + kn * a.cref_stride, rowbytes);
@@ -1384,7 +1398,7 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
       if (a.g) l2_prefetch(a.g + (rowbase + 1) * n, rowbytes * (uint32_t)(a.n_fsteps + (a.tail ? 1 : 0)));
     }
     __syncthreads();
-    int cur = 0;
+    int cur = start_buf;
     for (int j = 1; j <= a.n_fsteps; ++j) {
       double* src = row0 + cur * PS;
       double* dst = row0 + (cur ^ 1) * PS;
@@ -1405,8 +1419,9 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
         slice_to_global<P>(dst, a.u + (rowbase + j) * n, n, S);
     }
     if (a.tail) {  // one more step from the last F-point, into the free buffer
-      const double* src = row0 + cur * PS;
+      double* const src = row0 + cur * PS;  // free after the step: next start row (chain)
       double* zb = row0 + (cur ^ 1) * PS;
+      const bool hand = chain && k + 1 < kb1;
       if (own) win_step<P, SPAN, EXACT>(src, zb, t, T, S, tb, r0, wd);
       __syncthreads();
       const long long grow = rowbase + a.m;
@@ -1441,6 +1456,11 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
               cc.x = __dadd_rn(cc.x, ce[u].x);
               cc.y = __dadd_rn(cc.y, ce[u].y);
             }
+            if (hand) {  // == the next head's C_{k+1} (+ e_{k+1})
+              src[saddr<P>(i, S)] = cc.x;
+              src[saddr<P>(i + 1, S)] = cc.y;
+              if (a.c_out) *reinterpret_cast<double2*>(a.c_out + (k + 1) * a.c_out_stride + i) = cc;
+            }
             const double2 r = make_double2(__dsub_rn(z.x, cc.x), __dsub_rn(z.y, cc.y));
             part = fma(r.x, r.x, part);
             part = fma(r.y, r.y, part);
@@ -1448,6 +1468,7 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
           }
         }
       }
+      if (hand) have = cur;
       if (a.tail == 2 && a.partials) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
