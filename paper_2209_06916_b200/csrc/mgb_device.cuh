@@ -1392,8 +1392,9 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
       if (kn < kb1) {
         if (a.c_src) l2_prefetch(a.c_src + kn * a.c_stride, rowbytes);
         if (a.e) l2_prefetch(a.e + kn * a.e_stride, rowbytes);
-        if (a.tail == 2 && a.cref) l2_prefetch(a.cref + kn * a.cref_stride, rowbytes);
-        if (a.tail == 2 && a.cref_e) l2_prefetch(a.cref_e + kn * a.cref_e_stride, rowbytes);
+        // chained passes: cref[k] == c_src[k+1], already prefetched above
+        if (!chain && a.tail == 2 && a.cref) l2_prefetch(a.cref + kn * a.cref_stride, rowbytes);
+        if (!chain && a.tail == 2 && a.cref_e) l2_prefetch(a.cref_e + kn * a.cref_e_stride, rowbytes);
       }
       if (a.g) l2_prefetch(a.g + (rowbase + 1) * n, rowbytes * (uint32_t)(a.n_fsteps + (a.tail ? 1 : 0)));
     }
