@@ -1279,7 +1279,11 @@ template <int P, int SPAN, bool EXACT>
 __device__ __forceinline__ void win_step(const double* __restrict__ src, double* __restrict__ dst,
                                          int t, int T, int S, int tb, int r0,
                                          const double (&wd)[SPAN + 1]) {
-  constexpr int H = P >= 8 ? P / 2 : P;  // outputs per pass (window of H + SPAN in registers)
+#ifndef MGB_WIN_HDIV
+#define MGB_WIN_HDIV 2
+#endif
+  // outputs per pass (window of H + SPAN in registers)
+  constexpr int H = P >= 4 * MGB_WIN_HDIV ? P / MGB_WIN_HDIV : (P >= 8 ? P / 2 : P);
 #pragma unroll
   for (int h = 0; h < P; h += H) {
     double win[H + SPAN];
