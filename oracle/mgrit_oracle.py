@@ -174,12 +174,13 @@ def _dot_rows_reordered(a, b, block=256):
     return out
 
 
-def gmres_rows(op, B, tol, cap, reduction="reference"):
+def gmres_rows(op, B, tol, cap, reduction="reference", stats=None):
     """Per-row unrestarted GMRES(x0 = 0), circulant.py:262-332.
 
     ``reduction="reordered"`` swaps every dot product / norm for a blocked,
     reversed-order sum: the oracle's self-noise calibration run (SURVEY 0.6,
-    8c).  Returns (X, relative residuals, columns used, breakdown flag).
+    8c).  Returns (X, relative residuals, columns used, breakdown flag);
+    ``stats`` (a dict, optional) receives the per-row depth and residual.
     """
     if reduction == "reference":
         rowdot = lambda a, b: np.einsum("kn,kn->k", a, b)          # :297
@@ -193,6 +194,8 @@ def gmres_rows(op, B, tol, cap, reduction="reference"):
     live = beta > 0.0
     X = np.zeros_like(B)
     if not np.any(live):
+        if stats is not None:
+            stats.update(depth=np.zeros(K, dtype=int), res=np.zeros(K))
         return X, np.zeros(K), 0, False
     V = np.zeros((K, cap + 1, n))
     H = np.zeros((K, cap + 1, cap))
@@ -239,6 +242,8 @@ def gmres_rows(op, B, tol, cap, reduction="reference"):
         if jk:
             y = np.linalg.solve(H[k, :jk, :jk], g[k, :jk])
             X[k] = y @ V[k, :jk, :]
+    if stats is not None:
+        stats.update(depth=used.copy(), res=res.copy())
     return X, res, j, broke
 
 

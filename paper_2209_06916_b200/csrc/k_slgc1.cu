@@ -9,9 +9,13 @@ namespace mgb {
                   reinterpret_cast<const void*>(&relax_cl1_kernel<SEGK, CAP, R, NWMAX>))
 // reach R of (I - phi D^(p+1)): p = 1 -> 1 (cap 10), p = 3 -> 2, p = 5 -> 3 (cap 20);
 // NWMAX vector warps per CTA (8: 288 threads, 16: 544 threads with 64-point segments)
+// (key 108: every basis row resident; key 109: rows beyond the shared-memory
+// budget in the CTA's L2-resident workspace slot)
 #define REG_CL1B(SEGK, CAP, R)                                                           \
   register_kernel(KernelKey{K_SLGC1, SEGK, CAP, R, 108},                                 \
-                  reinterpret_cast<const void*>(&relax_cl1_kernel<SEGK, CAP, R, 8, 2>))
+                  reinterpret_cast<const void*>(&relax_cl1_kernel<SEGK, CAP, R, 8, 2>)); \
+  register_kernel(KernelKey{K_SLGC1, SEGK, CAP, R, 109},                                 \
+                  reinterpret_cast<const void*>(&relax_cl1_kernel<SEGK, CAP, R, 8, 2, true>))
 void register_slgc1() {
   // two CTAs per SM (<= 112 registers): single-wave launches of mid-sized levels
   REG_CL1B(2, 20, 2);

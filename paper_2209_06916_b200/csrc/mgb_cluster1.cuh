@@ -225,11 +225,12 @@ __device__ __forceinline__ double c1_sl(const C1Ctx& c, cg::cluster_group& cl, i
 // i <= j: V_i.u, lane j+1: u.u, lane j+2: u.Au (u = vx[3r..], Au = zx[3r..]).
 // No shuffles; 16-byte loads of rows whose stride is 2 (mod 4) doubles
 // (conflict-free), u broadcast.
+template <bool OVF>
 __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
   const int lane = c.lane, S = c.S, off = 3 * c.r;
   if (lane <= j + 2) {
     const double* uu = c.vx + off;
-    const double* vr = lane <= j ? c1_row<false>(c, lane) + c.seg : (lane == j + 1 ? uu : c.zx + off);
+    const double* vr = lane <= j ? c1_row<OVF>(c, lane) + c.seg : (lane == j + 1 ? uu : c.zx + off);
     const double2* v2 = reinterpret_cast<const double2*>(vr);
     const double2* u2 = reinterpret_cast<const double2*>(uu);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -246,7 +247,7 @@ __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
 
 // Wide segments (SEGK >= 4): lane-parallel products over the lane's own points,
 // then fixed-order warp butterflies, four rows interleaved.  Rows as c1_dots.
-template <int SEGK>
+template <int SEGK, bool OVF>
 __device__ __forceinline__ void c1_dots_lanes(C1Ctx& c, int j) {
   const int lane = c.lane, off = 3 * c.r;
   double uo[SEGK], ao[SEGK];
@@ -262,7 +263,7 @@ __device__ __forceinline__ void c1_dots_lanes(C1Ctx& c, int j) {
       const int i = i0 + ii;
       double s = 0.0;
       if (i <= j) {
-        const double* vr = c1_row<(SEGK >= 4)>(c, i) + c.seg + lane;
+        const double* vr = c1_row<OVF>(c, i) + c.seg + lane;
 #pragma unroll
         for (int k = 0; k < SEGK; ++k) s = fma(vr[32 * k], uo[k], s);
       } else if (i == j + 1) {
@@ -302,7 +303,7 @@ __device__ __forceinline__ void c1_dots_lanes(C1Ctx& c, int j) {
 // Whatever the first pass leaves in span(V) is O(eps) and is removed by the
 // full second pass one step later, so H and the basis agree with the
 // reference's MGS GMRES (circulant.py:262-332) to rounding.
-template <int SEGK, int CAP, int R, int NWMAX>
+template <int SEGK, int CAP, int R, int NWMAX, bool OVF>
 __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int& depth_out,
                         double& res_out) {
   const C1Params& P = *c.p;
@@ -342,7 +343,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       c.zx[xx] = c1_A<R>(w2, c.vx, xx);
     }
     __syncwarp();
-    if constexpr (SEGK >= 4) c1_dots_lanes<SEGK>(c, -1); else c1_dots(c, -1);  // rows: b.b, b.Ab
+    if constexpr (SEGK >= 4) c1_dots_lanes<SEGK, OVF>(c, -1); else c1_dots<OVF>(c, -1);  // rows: b.b, b.Ab
   }
   CL_TR(8)
   __syncthreads();
@@ -406,7 +407,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
             for (int ii = 0; ii < 4; ++ii) {
               const int i = i0 + ii;
               const double a_b = i < j ? coef[i] : 0.0;
-              const double* Vi = c1_row<(SEGK >= 4)>(c, i < j ? i : 0) + e0;
+              const double* Vi = c1_row<OVF>(c, i < j ? i : 0) + e0;
 #pragma unroll
               for (int k = 0; k < KX; ++k) {
                 const int xx = lane + 32 * k;
@@ -496,7 +497,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       // ---- vector warps: v_j, u_{j+1} = A v_j - hn v_{j-1} - hj v_j, A u_{j+1}, dots
       double* Un = c.U + (pu ^ 1) * LD + c.HW;
       const double inv = coef[CAP];
-      double* Vj = c1_row<(SEGK >= 4)>(c, j);
+      double* Vj = c1_row<OVF>(c, j);
 #pragma unroll
       for (int k = 0; k < KX; ++k) {
         const int xx = lane + 32 * k;
@@ -511,7 +512,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       double u[KX];
       {
         const double hj = coef[CAP + 1], hb = coef[CAP + 2];
-        const double* Vp = c1_row<(SEGK >= 4)>(c, j > 0 ? j - 1 : 0) + e0;
+        const double* Vp = c1_row<OVF>(c, j > 0 ? j - 1 : 0) + e0;
 #pragma unroll
         for (int k = 0; k < KX; ++k) {
           const int xx = lane + 32 * k;
@@ -551,7 +552,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
         c.zx[xx] = c1_A<R>(w2, c.vx, xx);
       }
       __syncwarp();
-      if constexpr (SEGK >= 4) c1_dots_lanes<SEGK>(c, j); else c1_dots(c, j);
+      if constexpr (SEGK >= 4) c1_dots_lanes<SEGK, OVF>(c, j); else c1_dots<OVF>(c, j);
       CL_TR(4)
     }
     __syncthreads();
@@ -594,7 +595,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
     for (int i = 0; i < depth; ++i) {
       const double yi = c.ybuf[i];
 #pragma unroll
-      for (int k = 0; k < SEGK; ++k) x[k] = fma(yi, c1_row<(SEGK >= 4)>(c, i)[c.seg + lane + 32 * k], x[k]);
+      for (int k = 0; k < SEGK; ++k) x[k] = fma(yi, c1_row<OVF>(c, i)[c.seg + lane + 32 * k], x[k]);
     }
   }
   CL_TR(7)
@@ -637,7 +638,9 @@ __device__ __forceinline__ double c1_sum_to_rank0(C1Ctx& c, double v) {
 
 // Interval relaxation with corrected SL steps, one cluster per interval, same
 // argument semantics as relax_kernel / relax_cluster_kernel (mgb_relax_args).
-template <int SEGK, int CAP, int R, int NWMAX, int MINB = 1>
+// OVF: basis rows K..CAP-1 may live in the CTA's workspace slot (K < CAP when
+// the rows do not all fit the shared-memory budget of the build)
+template <int SEGK, int CAP, int R, int NWMAX, int MINB = 1, bool OVF = (SEGK >= 4)>
 __global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
     relax_cl1_kernel(const StepParams* __restrict__ gp, const RelaxLaunch L) {
   cg::cluster_group cl = cg::this_cluster();
@@ -687,7 +690,8 @@ __global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
   c.vec = c.warp < NW;
   c.V = sm + LY.V + (P.HW & 1);  // c.V + HW (own point 0 of row 0) is 16-byte aligned
   c.K = P.K;
-  c.Vg = L.ws ? L.ws + (size_t)blockIdx.x * (size_t)(CAP - P.K) * P.LD : nullptr;
+  // overflow rows share the resident rows' alignment shift (16-byte row loads)
+  c.Vg = L.ws ? L.ws + (size_t)blockIdx.x * (size_t)(CAP - P.K) * P.LD + (P.HW & 1) : nullptr;
   c.U = sm + LY.U;
   c.in_row = sm + LY.in_row;
   const int XS = c1_xs(P.S, P.r);
@@ -747,7 +751,7 @@ __global__ void __launch_bounds__(32 * (NWMAX + 1), MINB)
     const int nsteps = a.n_fsteps + (a.tail ? 1 : 0);
     for (int j = 1; j <= nsteps; ++j) {
       const bool is_tail = j > a.n_fsteps;
-      c1_step<SEGK, CAP, R, NWMAX>(c, cl, y, depth, gres);
+      c1_step<SEGK, CAP, R, NWMAX, OVF>(c, cl, y, depth, gres);
       const long long grow = is_tail ? rowbase + a.m : rowbase + j;
       if (!is_tail) {
         if (c.vec) {

@@ -46,14 +46,18 @@ std::map<std::tuple<int, int, int, int, int>, const void*>& registry() {
   static std::map<std::tuple<int, int, int, int, int>, const void*> r;
   return r;
 }
-// The max-dynamic-shared-memory attribute belongs to the kernel FUNCTION, which
-// several plans (different n_x) share: only ever raise it, so a later smaller
-// plan cannot invalidate the launches of an earlier larger one.
+// The max-dynamic-shared-memory attribute belongs to the kernel FUNCTION on the
+// current device, which several plans (different n_x) share: only ever raise
+// it, so a later smaller plan cannot invalidate the launches of an earlier
+// larger one.  Tracked per (device, function).
 cudaError_t raise_smem_attr(const void* fn, int bytes) {
   static std::mutex mu;
-  static std::map<const void*, int> cur;
+  static std::map<std::pair<int, const void*>, int> cur;
+  int dev = 0;
+  const cudaError_t ed = cudaGetDevice(&dev);
+  if (ed != cudaSuccess) return ed;
   std::lock_guard<std::mutex> lk(mu);
-  int& have = cur[fn];
+  int& have = cur[std::make_pair(dev, fn)];
   if (bytes <= have) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) have = bytes;
@@ -433,10 +437,17 @@ void prepare_clusters1(mgb_step* st) {
     if (!segk || 3 * r > nc) continue;
     for (int occ2 = 0; occ2 < 2; ++occ2) {
       if (occ2 && !(nwmax == 8 && segk == 2 && capt == 20 && r >= 2)) continue;
+      const size_t budget = occ2 ? 113 * 1024 : 227 * 1024;
+      int K = capt;
+      while (K > 1 && mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt, K) > budget) --K;
+      // basis rows beyond K live in a workspace slot: only builds compiled for it
+      // (wide segments; the 2-CTA/SM overflow build, key 109)
+      if (K < capt && segk < 4 && !occ2) continue;
+      const int key = occ2 ? (K < capt ? 109 : 108) : nwmax;
       const void* fn = nullptr;
       {
         std::lock_guard<std::mutex> lk(reg_mutex());
-        auto it = registry().find(std::make_tuple((int)mgb::K_SLGC1, segk, capt, r, occ2 ? 108 : nwmax));
+        auto it = registry().find(std::make_tuple((int)mgb::K_SLGC1, segk, capt, r, key));
         if (it == registry().end()) continue;
         fn = it->second;
       }
@@ -447,9 +458,6 @@ void prepare_clusters1(mgb_step* st) {
       v.fn = fn;
       v.one_red = true;
       v.occ = occ2 ? 2 : 1;
-      const size_t budget = occ2 ? 113 * 1024 : 227 * 1024;
-      int K = capt;
-      while (K > 1 && mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt, K) > budget) --K;
       v.K = K;
       v.smem = (int)mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt, K);
       if ((size_t)v.smem > budget) continue;
@@ -460,7 +468,8 @@ void prepare_clusters1(mgb_step* st) {
       if (!ok) continue;
       if (K < capt) {  // overflow rows: one slot of (cap - K) halo'd rows per resident CTA
         const size_t rows = (size_t)(capt - K) * mgb::c1_ld(nc, r);
-        if (cudaMalloc(&v.ws, rows * 8 * (size_t)v.max_clusters * C) != cudaSuccess) {
+        // + one double: the slots share the resident rows' 16-byte alignment shift
+        if (cudaMalloc(&v.ws, rows * 8 * (size_t)v.max_clusters * C + 16) != cudaSuccess) {
           cudaGetLastError();
           continue;
         }
