@@ -97,6 +97,7 @@ class Engine:
     def fr(self, l, u, g, src, gn, k0, nb, u_zero): raise NotImplementedError
     def cf(self, l, u, g, src, e, k0, nb, u_zero, want_norm): raise NotImplementedError
     def coarse_solve(self, level, g_full, kind): raise NotImplementedError  # rank 0
+    def ordered_sum(self, allp): raise NotImplementedError  # rank 0: (1,) comm tensor
 
 
 class GpuEngine(Engine):
@@ -111,6 +112,34 @@ class GpuEngine(Engine):
         self.plans = [plan_for(problem.steppers[l].program) for l in range(len(self.m))]
         self.zero_row = self.torch.zeros(self.n, dtype=self.torch.float64, device="cuda")
         self._coarse = None
+        #: set to a list to record (name, start_event, end_event) per launch
+        self.profile = None
+
+    def _relax(self, name, l, *args, **kw):
+        if self.profile is None:
+            return self.plans[l].relax(*args, **kw)
+        ev = [self.torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        self.plans[l].relax(*args, **kw)
+        ev[1].record()
+        self.profile.append((name, ev[0], ev[1]))
+
+    def profile_summary(self) -> dict:
+        """{pass name: (launches, total ms)} of the recorded launches."""
+        self.torch.cuda.synchronize()
+        out = {}
+        for name, s, e in self.profile or []:
+            cnt, ms = out.get(name, (0, 0.0))
+            out[name] = (cnt + 1, ms + s.elapsed_time(e))
+        return out
+
+    def ordered_sum(self, allp):
+        """mgb_sum over the partials in global interval order: the single-GPU
+        solver's fixed-order tree, so the history is bitwise the single-GPU one."""
+        from .device import device_sum
+        out = self.torch.empty(1, dtype=self.torch.float64, device="cuda")
+        device_sum(allp.data_ptr(), allp.numel(), out.data_ptr())
+        return out
 
     def zeros(self, rows):
         return self.torch.zeros((rows, self.n), dtype=self.torch.float64, device="cuda")
@@ -127,8 +156,8 @@ class GpuEngine(Engine):
     def initial_partials(self, u_loc, nb):
         part = self.torch.empty(nb, dtype=self.torch.float64, device="cuda")
         m, n = self.m[0], self.n
-        self.plans[0].relax(nb, m, 0, c_src=self._p(u_loc, m - 1), c_stride=m * n, tail=2,
-                            cref=self._p(u_loc, m), cref_stride=m * n, partials=part.data_ptr())
+        self._relax("L0.R", 0, nb, m, 0, c_src=self._p(u_loc, m - 1), c_stride=m * n, tail=2,
+                    cref=self._p(u_loc, m), cref_stride=m * n, partials=part.data_ptr())
         return part
 
     def _src(self, l, u, src, u_zero):
@@ -141,9 +170,9 @@ class GpuEngine(Engine):
     def fc(self, l, u, g, src, cb, k0, nb, u_zero):
         m, n = self.m[l], self.n
         c_src, stride, u0row = self._src(l, u, src, u_zero)
-        self.plans[l].relax(nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
-                            c_src0=u0row, tail=1, tail_out=self._p(cb, 1), tail_stride=n,
-                            g=self._p(g))
+        self._relax(f"L{l}.FC", l, nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
+                    c_src0=u0row, tail=1, tail_out=self._p(cb, 1), tail_stride=n,
+                    g=self._p(g))
 
     def fr(self, l, u, g, src, gn, k0, nb, u_zero):
         m, n = self.m[l], self.n
@@ -153,26 +182,26 @@ class GpuEngine(Engine):
                                  else (self._p(u, m), m * n))
         else:
             cref, cref_stride = self._p(src, 1), n
-        self.plans[l].relax(nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
-                            c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
-                            tail_out=self._p(gn, 1), tail_stride=n, g=self._p(g))
+        self._relax(f"L{l}.FR", l, nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
+                    c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
+                    tail_out=self._p(gn, 1), tail_stride=n, g=self._p(g))
 
     def cf(self, l, u, g, src, e, k0, nb, u_zero, want_norm):
         m, n = self.m[l], self.n
         c_src, stride, u0row = self._src(l, u, src, u_zero)
         fuse = want_norm and src is not None
         part = self.torch.empty(nb, dtype=self.torch.float64, device="cuda") if want_norm else None
-        self.plans[l].relax(nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
-                            c_src0=u0row, e=self._p(e), e_stride=n, c_out=self._p(u),
-                            c_out_stride=m * n, c_last_out=self._p(u, nb * m), u=self._p(u),
-                            write_f=2, g=self._p(g), tail=2 if fuse else 0,
-                            cref=(c_src + n * _F64) if fuse else None, cref_stride=n,
-                            cref_e=self._p(e, 1), cref_e_stride=n,
-                            partials=part.data_ptr() if fuse else None)
+        self._relax(f"L{l}.CF", l, nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
+                    c_src0=u0row, e=self._p(e), e_stride=n, c_out=self._p(u),
+                    c_out_stride=m * n, c_last_out=self._p(u, nb * m), u=self._p(u),
+                    write_f=2, g=self._p(g), tail=2 if fuse else 0,
+                    cref=(c_src + n * _F64) if fuse else None, cref_stride=n,
+                    cref_e=self._p(e, 1), cref_e_stride=n,
+                    partials=part.data_ptr() if fuse else None)
         if want_norm and not fuse:
-            self.plans[l].relax(nb, m, 0, c_src=self._p(u, m - 1), c_stride=m * n, tail=2,
-                                cref=self._p(u, m), cref_stride=m * n, g=self._p(g),
-                                partials=part.data_ptr())
+            self._relax("L0.R", l, nb, m, 0, c_src=self._p(u, m - 1), c_stride=m * n, tail=2,
+                        cref=self._p(u, m), cref_stride=m * n, g=self._p(g),
+                        partials=part.data_ptr())
         return part
 
     def coarse_solve(self, level, g_full, kind):
@@ -180,8 +209,10 @@ class GpuEngine(Engine):
             self._coarse = MgritSolver(self.problem, self.config)
             self._coarse._build()
         s = self._coarse
+        s.profile = self.profile
         s.gcoarse[level].copy_(g_full)
         s._coarse_solve(level, kind)
+        s.profile = None
         return s.ucoarse[level]
 
 
@@ -238,23 +269,26 @@ class ShardedMgritSolver:
 
     # --------------------------------------------------------- exchanges
     def _pass_right(self, cb, nb):
-        """cb[nb] (my last C-relaxed point) -> the right neighbour's cb[0]."""
+        """cb[nb] (my last C-relaxed point) -> the right neighbour's cb[0]
+        (non-blocking send and receive, both posted before either waits)."""
         import torch
         if self.world == 1:
             return
         eng, dist = self.engine, self.dist
         reqs = []
-        if self.rank + 1 < self.world:
-            reqs.append(dist.isend(eng.to_comm(cb[nb:nb + 1]).contiguous(), self.rank + 1,
-                                   group=self.group))
+        recv = None
         if self.rank > 0:
             first = eng.to_comm(cb[0:1])
             recv = torch.empty_like(first)
-            dist.recv(recv, self.rank - 1, group=self.group)
-            first.copy_(recv)
-            cb[0:1] = eng.from_comm(first, cb[0:1])
+            reqs.append(dist.irecv(recv, self.rank - 1, group=self.group))
+        if self.rank + 1 < self.world:
+            reqs.append(dist.isend(eng.to_comm(cb[nb:nb + 1]).contiguous(), self.rank + 1,
+                                   group=self.group))
         for r in reqs:
             r.wait()
+        if recv is not None:
+            first.copy_(recv)
+            cb[0:1] = eng.from_comm(first, cb[0:1])
 
     def _gather_solve_scatter(self, level, gn, nb, kind):
         """Rows 1..nb of every rank's gn -> rank 0 (row 0 = 0), which solves
@@ -315,20 +349,23 @@ class ShardedMgritSolver:
         return e
 
     def _global_sum(self, part) -> float:
-        """Fixed-order sum of per-interval partials over all ranks (bitwise
-        independent of the number of ranks)."""
+        """Sum of the per-interval partials of all ranks: gathered in global
+        interval order into one buffer on rank 0 and reduced there by the
+        engine's fixed-order sum (GPU: the single-GPU solver's ``mgb_sum``
+        tree), so the history is bitwise independent of the number of ranks."""
         import torch
         eng, dist = self.engine, self.dist
-        t = eng.to_comm(part)
+        t = eng.to_comm(part).contiguous()
         if self.world > 1:
             bufs = [torch.empty_like(t) for _ in range(self.world)] if self.rank == 0 else None
             dist.gather(t, bufs, dst=0, group=self.group)
             allp = torch.cat(bufs) if self.rank == 0 else None
         else:
             allp = t
-        tot = torch.zeros(1, dtype=torch.float64, device=t.device)
         if self.rank == 0:
-            tot[0] = _ordered_sum(allp)
+            tot = eng.ordered_sum(allp)
+        else:
+            tot = torch.zeros(1, dtype=torch.float64, device=t.device)
         if self.world > 1:
             dist.broadcast(tot, src=0, group=self.group)
         return math.sqrt(float(tot.item()))
@@ -366,11 +403,3 @@ def initial_rows(seed: int, r0: int, r1: int, n_x: int, u0) -> np.ndarray:
         u[0] = u0
     return u
 
-
-def _ordered_sum(t) -> float:
-    """Sequential sum in interval order (host side, exact same order for any
-    rank count)."""
-    acc = 0.0
-    for v in t.detach().cpu().numpy().tolist():
-        acc += v
-    return acc

@@ -104,6 +104,25 @@ class OracleEngine(Engine):
         r = (self._g(g, m, m, nb) + st.apply(X)) - C[1:nb + 1]
         return np.array([float(np.dot(x, x)) for x in r])
 
+    def ordered_sum(self, allp):
+        """mgb_sum's order (csrc/mgb_host.cu sum_kernel) restated: 1024 threads
+        each sum every 1024th partial in order, a xor-butterfly inside each warp,
+        then the 32 warp totals in order."""
+        p = allp.numpy()
+        acc = np.zeros(1024)
+        for start in range(0, len(p), 1024):
+            blk = np.zeros(1024)
+            blk[:len(p) - start if len(p) - start < 1024 else 1024] = p[start:start + 1024]
+            acc = acc + blk
+        tot = 0.0
+        lane = np.arange(32)
+        for w in range(32):
+            v = acc[32 * w:32 * w + 32].copy()
+            for o in (16, 8, 4, 2, 1):
+                v = v + v[lane ^ o]
+            tot += v[0]
+        return torch.tensor([tot], dtype=torch.float64)
+
     def coarse_solve(self, level, gc, kind):
         if kind == "two_level" or level == len(self.factors):
             return O.forward_substitute(self.steps[level], gc)

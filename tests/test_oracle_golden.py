@@ -199,6 +199,40 @@ def test_baseline_config_histories_recorded():
             assert HIST[k]["iterations"] == v and HIST[k]["converged"]
 
 
+def test_oracle_full_size_cfg1_bitwise():
+    """The oracle reproduces the real reference's full-size cfg1 run
+    (tests/golden/full, make_full.py) bit for bit: history and final iterate."""
+    from paper_2209_06916_b200.configs import CONFIGS, seeded_u0
+    ref = json.load(open(os.path.join(HERE, "full", "cfg1.json")))
+    fin = np.load(os.path.join(HERE, "full", "cfg1_final.npz"))
+    from threadpoolctl import threadpool_limits
+    cf = CONFIGS["cfg1"]
+    steps, fac, _ = O.build_hierarchy(cf.family, cf.p, cf.c, cf.n_x, cf.n_t, cf.m, cf.cycle)
+    # make_full.py runs the reference with one BLAS thread: a threaded ddot
+    # (np.linalg.norm, mgrit.py:166) sums in another order (last-bit norms)
+    with threadpool_limits(1):
+        out = O.Mgrit(steps, fac, cf.n_t, seeded_u0(cf.u0, cf.n_x), cycle=cf.cycle).solve()
+    assert out["norms"] == ref["norms"] and out["iterations"] == ref["iterations"]
+    assert _same(out["u"][fin["rows"]], fin["samples"])
+
+
+def test_full_size_reference_runs_recorded():
+    """Every full-size / proxy reference run has the reference's histories.json
+    iteration count, and the full-size runs repeat histories.json's history
+    (to the last bits: those runs used a multithreaded BLAS ddot in the norm)."""
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg4p", "cfg5p"):
+        path = os.path.join(HERE, "full", name + ".json")
+        if not os.path.exists(path):
+            continue
+        rec = json.load(open(path))
+        assert rec["converged"]
+        if name in HIST:
+            assert rec["iterations"] == HIST[name]["iterations"]
+            r0 = rec["norms"][0]
+            np.testing.assert_allclose(rec["norms"], HIST[name]["norms"], rtol=0,
+                                       atol=1e-13 * r0)
+
+
 # --------------------------------------------------------------- validation
 
 def test_config_and_problem_validation():
