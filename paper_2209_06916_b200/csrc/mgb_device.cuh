@@ -86,6 +86,9 @@ struct RelaxLaunch {
   mgb_relax_args a;
   double* ws;            // GMRES workspace base (slot = blockIdx.x)
   long long ws_slot;     // doubles per slot
+  // register-window stencil weights (relax_win_kernel): kernel parameters live in
+  // the constant bank, so every tap weight is an instruction operand, not a register
+  double win_w[32];
 };
 
 // ---------------------------------------------------------------- helpers
@@ -1270,52 +1273,100 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __r
 
 // ------------------------------------------- explicit-stencil relaxation
 // Dedicated kernel for assembled explicit stencils (the fine ERK levels):
-// stencil weights and geometry live in registers (no shared parameter copy),
+// stencil weights are kernel parameters (constant-bank operands, no registers),
 // the resident slice is double-buffered (one CTA barrier per step), outputs
-// are produced in half-chunks straight into the other buffer (fewer live
-// registers -> 3 CTAs/SM), rows stream to HBM with 16-byte stores.  Same
-// argument semantics as relax_kernel (mgb_relax_args).
-template <int P, int SPAN, bool EXACT>
+// are produced in part-chunks straight into the other buffer (few live
+// registers: 2 CTAs/SM at 256 threads, 1 CTA/SM at 512), rows stream to HBM
+// with 16-byte stores issued from INSIDE the next step's stencil arithmetic
+// (the row just completed is that step's read-only source), so the store
+// traffic overlaps the FP64 work instead of following it.  Same argument
+// semantics as relax_kernel (mgb_relax_args).
+template <int P>
+__device__ __forceinline__ void slice_store2(const double* row, double* dst, int i, int S) {
+  // elements i, i+1 (i even: same chunk column pair), natural order, streaming
+  const int s0 = saddr<P>(i, S);
+  __stcs(reinterpret_cast<double2*>(dst + i), make_double2(row[s0], row[s0 + S]));
+}
+
+// Fixed-geometry builds (TT = threads = chunks, compile time): the slice row
+// stride is the constant WIN_S<TT> and every chunk row is extended by WIN_X
+// columns that replicate columns 0..WIN_X-1 (the periodic wrap), so a window
+// read is base + immediate: no wrap arithmetic and no address registers.
+constexpr int WIN_X = 4;
+template <int TT>
+struct WinGeo {
+  static constexpr int S = TT + 17;  // == 1 (mod 16): conflict-free rows and natural-order copies
+};
+template <int P, int TT>
+__device__ __forceinline__ void slice_put(double* row, int i, double v, int S) {
+  const int s = saddr<P>(i, S);
+  row[s] = v;
+  if (TT > 0 && i < WIN_X * P) row[s + TT] = v;  // wrap replica
+}
+
+// One stencil step src -> dst.  ``gdst`` (may be null): natural-order global copy
+// of the SOURCE row, issued in pieces between the outputs.
+template <int P, int SPAN, bool EXACT, int TT>
 __device__ __forceinline__ void win_step(const double* __restrict__ src, double* __restrict__ dst,
                                          int t, int T, int S, int tb, int r0,
-                                         const double (&wd)[SPAN + 1]) {
-#ifndef MGB_WIN_HDIV
-#define MGB_WIN_HDIV 2
-#endif
+                                         const double (&wd)[SPAN + 1], double* __restrict__ gdst, int n, int nthr,
+                                         bool own) {
   // outputs per pass (window of H + SPAN in registers)
-  constexpr int H = P >= 4 * MGB_WIN_HDIV ? P / MGB_WIN_HDIV : (P >= 8 ? P / 2 : P);
+  // (4 measured fastest on B200 for spans 9 and 30 at 16 points per thread: 8 and 16
+  // trade fewer shared loads for register spills)
+#ifndef MGB_WIN_H
+#define MGB_WIN_H 4
+#endif
+  constexpr int H = MGB_WIN_H < P ? MGB_WIN_H : P;
+  static_assert(TT == 0 || (P - 1 + P - 1 + SPAN) / P < WIN_X, "wrap replica too narrow");
+  int gi = 2 * t;  // next natural-order element pair this thread copies
 #pragma unroll
   for (int h = 0; h < P; h += H) {
     double win[H + SPAN];
+    if (own) {
 #pragma unroll
-    for (int w = 0; w < H + SPAN; ++w) {
-      const int cw = r0 + h + w;
-      int tt = tb + cw / P;
-      tt = tt >= T ? tt - T : tt;
-      tt = tt >= T ? tt - T : tt;
-      win[w] = src[(cw & (P - 1)) * S + tt];
+      for (int w = 0; w < H + SPAN; ++w) {
+        const int cw = r0 + h + w;
+        if constexpr (TT > 0) {
+          win[w] = src[(cw & (P - 1)) * WinGeo<TT>::S + cw / P + tb];
+        } else {
+          int tt = tb + cw / P;
+          tt = tt >= T ? tt - T : tt;
+          tt = tt >= T ? tt - T : tt;
+          win[w] = src[(cw & (P - 1)) * S + tt];
+        }
+      }
     }
 #pragma unroll
     for (int q = 0; q < H; ++q) {
-      // numpy starts from zeros: 0 + w0*v0 == w0*v0 (up to the sign of an exact zero)
-      double acc = EXACT ? __dmul_rn(wd[0], win[q]) : wd[0] * win[q];
+      if (own) {
+        // numpy starts from zeros: 0 + w0*v0 == w0*v0 (up to the sign of an exact zero)
+        double acc = EXACT ? __dmul_rn(wd[0], win[q]) : wd[0] * win[q];
 #pragma unroll
-      for (int k = 1; k <= SPAN; ++k) acc = madd<EXACT>(acc, wd[k], win[q + k]);
-      dst[(h + q) * S + t] = acc;
+        for (int k = 1; k <= SPAN; ++k) acc = madd<EXACT>(acc, wd[k], win[q + k]);
+        if constexpr (TT > 0) {
+          dst[(h + q) * WinGeo<TT>::S + t] = acc;
+          if (t < WIN_X) dst[(h + q) * WinGeo<TT>::S + TT + t] = acc;
+        } else {
+          dst[(h + q) * S + t] = acc;
+        }
+      }
+      if (gdst && ((h + q) & 1) && gi < n) {  // one 16-byte piece of the source row per two outputs
+        slice_store2<P>(src, gdst, gi, TT > 0 ? WinGeo<TT>::S : S);
+        gi += 2 * nthr;
+      }
     }
   }
+  if (gdst)
+    for (; gi < n; gi += 2 * nthr) slice_store2<P>(src, gdst, gi, TT > 0 ? WinGeo<TT>::S : S);
 }
 
 template <int P>
 __device__ __forceinline__ void slice_to_global(const double* row, double* dst, int n, int S) {
   // natural-order 16-byte stores (n even), streaming
-  for (int i = 2 * threadIdx.x; i < n; i += 2 * blockDim.x)
-    __stcs(reinterpret_cast<double2*>(dst + i), make_double2(row[saddr<P>(i, S)], row[saddr<P>(i + 1, S)]));
+  for (int i = 2 * threadIdx.x; i < n; i += 2 * blockDim.x) slice_store2<P>(row, dst, i, S);
 }
 
-#ifndef MGB_WIN_MINB
-#define MGB_WIN_MINB 2
-#endif
 #ifndef MGB_WIN_U
 #define MGB_WIN_U 4
 #endif
@@ -1325,16 +1376,16 @@ __device__ __forceinline__ void l2_prefetch(const void* g, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
 }
 
-template <int P, int SPAN, bool EXACT>
-__global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const StepParams* __restrict__ gp,
-                                                                      const RelaxLaunch L) {
+template <int P, int SPAN, bool EXACT, int MAXT = 256, int MINB = 2, int TT = 0>
+__global__ void __launch_bounds__(MAXT, MINB) relax_win_kernel(const StepParams* __restrict__ gp,
+                                                               const RelaxLaunch L) {
   // Natural-order global traffic: thread t touches elements 2t, 2t+1 (+2*blockDim) with
   // 16-byte coalesced accesses and scatters/gathers the slice layout in shared memory.
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int n = gp->n, T = gp->T, S = gp->S;
-  double wd[SPAN + 1];
+  const int n = gp->n, T = TT > 0 ? TT : gp->T, S = TT > 0 ? WinGeo<TT>::S : gp->S;
+  double wd[SPAN + 1];  // uniform values read from the parameter bank: uniform registers / operands
 #pragma unroll
-  for (int k = 0; k <= SPAN; ++k) wd[k] = gp->win_w[k];
+  for (int k = 0; k <= SPAN; ++k) wd[k] = L.win_w[k];
   const int t = threadIdx.x;
   const bool own = t < T;
   const int lo = gp->win_lo;
@@ -1345,7 +1396,7 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
   const int PS = P * S;
   double* red = row0 + 2 * PS;
   const mgb_relax_args& a = L.a;
-  const int nthr = blockDim.x;
+  const int nthr = TT > 0 ? TT : (int)blockDim.x;
   const uint32_t rowbytes = (uint32_t)n * 8u;
   // Contiguous interval blocks per CTA.  When the residual tail of interval k
   // reads exactly the rows the head of interval k+1 starts from (CF and FR
@@ -1385,8 +1436,8 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
             y[u].y = __dadd_rn(y[u].y, ev[u].y);
           }
           if (a.c_out) *reinterpret_cast<double2*>(a.c_out + k * a.c_out_stride + i) = y[u];
-          row0[saddr<P>(i, S)] = y[u].x;
-          row0[saddr<P>(i + 1, S)] = y[u].y;
+          slice_put<P, TT>(row0, i, y[u].x, S);
+          slice_put<P, TT>(row0, i + 1, y[u].y, S);
         }
       }
     }
@@ -1404,30 +1455,31 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
     }
     __syncthreads();
     int cur = start_buf;
+    double* pend = nullptr;  // global row of the F-point held by buffer `cur`, not yet stored
     for (int j = 1; j <= a.n_fsteps; ++j) {
       double* src = row0 + cur * PS;
       double* dst = row0 + (cur ^ 1) * PS;
-      if (own) win_step<P, SPAN, EXACT>(src, dst, t, T, S, tb, r0, wd);
+      win_step<P, SPAN, EXACT, TT>(src, dst, t, T, S, tb, r0, wd, pend, n, nthr, own);
       __syncthreads();  // dst complete; src free for step j+1's output
       if (a.g) {  // upd + g (mgrit.py:142), natural order, then republish
         const double* gr = a.g + (rowbase + j) * n;
         for (int i = 2 * t; i < n; i += 2 * nthr) {
           const double2 gv = __ldg(reinterpret_cast<const double2*>(gr + i));
           const int s0 = saddr<P>(i, S), s1 = saddr<P>(i + 1, S);
-          dst[s0] = __dadd_rn(dst[s0], gv.x);
-          dst[s1] = __dadd_rn(dst[s1], gv.y);
+          slice_put<P, TT>(dst, i, __dadd_rn(dst[s0], gv.x), S);
+          slice_put<P, TT>(dst, i + 1, __dadd_rn(dst[s1], gv.y), S);
         }
         __syncthreads();
       }
       cur ^= 1;
-      if (a.write_f == 2 || (a.write_f == 1 && j == a.n_fsteps))
-        slice_to_global<P>(dst, a.u + (rowbase + j) * n, n, S);
+      pend = (a.write_f == 2 || (a.write_f == 1 && j == a.n_fsteps)) ? a.u + (rowbase + j) * n : nullptr;
     }
+    if (!a.tail && pend) slice_to_global<P>(row0 + cur * PS, pend, n, S);
     if (a.tail) {  // one more step from the last F-point, into the free buffer
       double* const src = row0 + cur * PS;  // free after the step: next start row (chain)
       double* zb = row0 + (cur ^ 1) * PS;
       const bool hand = chain && k + 1 < kb1;
-      if (own) win_step<P, SPAN, EXACT>(src, zb, t, T, S, tb, r0, wd);
+      win_step<P, SPAN, EXACT, TT>(src, zb, t, T, S, tb, r0, wd, pend, n, nthr, own);
       __syncthreads();
       const long long grow = rowbase + a.m;
       double part = 0.0;
@@ -1462,8 +1514,8 @@ __global__ void __launch_bounds__(256, MGB_WIN_MINB) relax_win_kernel(const Step
               cc.y = __dadd_rn(cc.y, ce[u].y);
             }
             if (hand) {  // == the next head's C_{k+1} (+ e_{k+1})
-              src[saddr<P>(i, S)] = cc.x;
-              src[saddr<P>(i + 1, S)] = cc.y;
+              slice_put<P, TT>(src, i, cc.x, S);
+              slice_put<P, TT>(src, i + 1, cc.y, S);
               if (a.c_out) *reinterpret_cast<double2*>(a.c_out + (k + 1) * a.c_out_stride + i) = cc;
             }
             const double2 r = make_double2(__dsub_rn(z.x, cc.x), __dsub_rn(z.y, cc.y));

@@ -377,6 +377,94 @@ struct mgb_step {
 };
 
 namespace {
+// Launch choices are plan-time parameters with the defaults below.  The MGB_*
+// environment variables override them for tooling only (variant sweeps,
+// bisection, the chained-interval tests); they are read once per process.
+struct Tuning {
+  bool debug = false;
+  bool no_cluster = false;    // MGB_NO_CLUSTER: single-CTA GMRES on every level
+  bool cgs2 = false;          // MGB_CL_CGS2: previous two-reduction cluster kernel
+  int c1_c = 0;               // MGB_C1_C: force one cluster size
+  bool c1_no_occ2 = false;    // MGB_C1_NO_OCC2: no 2-CTA/SM cluster builds
+  bool c1_wide = false;       // MGB_C1_WIDE: allow wide-segment cluster builds
+  bool c1_no_split = false;   // MGB_C1_NO_SPLIT: no second launch for a partial last wave
+  long long c1_waves = 2;     // MGB_C1_WAVES: cluster waves beyond which the single-CTA kernel runs
+  long long cluster_waves = 2;  // MGB_CLUSTER_WAVES: same for the two-reduction kernel
+  int c1_segk = 1;            // MGB_C1_SEGK: smallest segment width considered
+  bool slg_no_occ2 = false;   // MGB_SLG_NO_OCC2: no 2-CTA/SM single-CTA GMRES build
+  bool rk_stencil = false;    // MGB_RK_STENCIL: SDIRK stage values by the stencil in fast mode too
+  long long max_grid = 0;     // MGB_MAX_GRID: cap the grid (tests: many intervals per CTA)
+};
+const Tuning& tuning() {
+  static const Tuning t = [] {
+    Tuning x;
+    auto flag = [](const char* k) { return std::getenv(k) != nullptr; };
+    auto num = [](const char* k, long long d) { const char* v = std::getenv(k); return v ? std::atoll(v) : d; };
+    x.debug = flag("MGB_DEBUG");
+    x.no_cluster = flag("MGB_NO_CLUSTER");
+    x.cgs2 = flag("MGB_CL_CGS2");
+    x.c1_c = (int)num("MGB_C1_C", 0);
+    x.c1_no_occ2 = flag("MGB_C1_NO_OCC2");
+    x.c1_wide = flag("MGB_C1_WIDE");
+    x.c1_no_split = flag("MGB_C1_NO_SPLIT");
+    x.c1_waves = num("MGB_C1_WAVES", 2);
+    x.cluster_waves = num("MGB_CLUSTER_WAVES", 2);
+    x.c1_segk = (int)num("MGB_C1_SEGK", 1);
+    x.slg_no_occ2 = flag("MGB_SLG_NO_OCC2");
+    x.rk_stencil = flag("MGB_RK_STENCIL");
+    x.max_grid = num("MGB_MAX_GRID", 0);
+    return x;
+  }();
+  return t;
+}
+
+// Arguments of the sub-pass over intervals [k0, k0 + cnt) of pass ``a``.
+mgb_relax_args sub_range(const mgb_relax_args& a, long long k0, long long cnt, int n) {
+  mgb_relax_args s = a;
+  s.n_intervals = cnt;
+  s.k_global0 = a.k_global0 + k0;
+  const long long rows = k0 * (long long)a.m * n;
+  if (s.c_src) s.c_src += k0 * a.c_stride;
+  if (s.e) s.e += k0 * a.e_stride;
+  if (s.c_out) s.c_out += k0 * a.c_out_stride;
+  if (s.u) s.u += rows;
+  if (s.g) s.g += rows;
+  if (s.tail_out) s.tail_out += k0 * a.tail_stride;
+  if (s.cref) s.cref += k0 * a.cref_stride;
+  if (s.cref_e) s.cref_e += k0 * a.cref_e_stride;
+  if (s.partials) s.partials += k0;
+  if (s.stats_depth) s.stats_depth += k0;
+  if (s.stats_res) s.stats_res += k0;
+  if (k0 + cnt < a.n_intervals) s.c_last_out = nullptr;
+  return s;
+}
+
+int launch_cluster1(mgb_step* st, const ClusterVariant& v, const mgb_relax_args& a, void* stream) {
+  if (a.n_intervals <= 0) return MGB_OK;
+  const long long ncl = std::min<long long>(a.n_intervals, v.max_clusters);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * v.C));
+  cfg.blockDim = dim3(v.T);
+  cfg.dynamicSmemBytes = v.smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = v.C;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  const StepParams* dpc = st->dp;
+  mgb::RelaxLaunch L1;
+  L1.a = a;
+  L1.ws = v.ws;         // overflow basis rows (nullptr: all resident)
+  L1.ws_slot = v.K;     // resident row count
+  void* cargs[] = {(void*)&dpc, (void*)&L1};
+  CUDA_TRY(cudaLaunchKernelExC(&cfg, v.fn, cargs));
+  g_launches++;
+  return MGB_OK;
+}
+
 // Cluster launch variants for SL_GMRES: C CTAs per interval, P <= 2 points per
 // thread, 32 <= T <= 256 threads per CTA, column cap 10 or 20.
 bool try_cluster_variant(ClusterVariant& v) {
@@ -427,7 +515,7 @@ void prepare_clusters1(mgb_step* st) {
     const int nc = n / C;
     int segk = 0, NW = 0, nwmax = 0;
     const int cand[6][2] = {{1, 8}, {2, 8}, {2, 16}, {4, 16}, {8, 8}, {8, 16}};
-    static const int min_segk = std::getenv("MGB_C1_SEGK") ? std::atoi(std::getenv("MGB_C1_SEGK")) : 1;
+    const int min_segk = tuning().c1_segk;
     for (const auto& cd : cand) {
       if (cd[0] < min_segk) continue;
       if (nc % (32 * cd[0])) continue;
@@ -462,7 +550,7 @@ void prepare_clusters1(mgb_step* st) {
       v.smem = (int)mgb::c1_smem_bytes(nc, NW, 32 * segk, r, C, capt, K);
       if ((size_t)v.smem > budget) continue;
       const bool ok = try_cluster_variant(v);
-      if (std::getenv("MGB_DEBUG"))
+      if (tuning().debug)
         fprintf(stderr, "[mgb] cl1 variant n=%d C=%d segk=%d T=%d occ2=%d K=%d smem=%d ok=%d max_clusters=%d\n", n,
                 C, segk, v.T, occ2, K, v.smem, (int)ok, v.max_clusters);
       if (!ok) continue;
@@ -611,7 +699,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
       // reference's z = cL y (stepping.py:374): the subtraction cancels on
       // smooth modes and biases them by ~1e-16 per step (a 3e-12 drift of
       // cfg3's final iterate over 16384 steps).
-      static const bool stencil_stages = std::getenv("MGB_RK_STENCIL") != nullptr;
+      const bool stencil_stages = tuning().rk_stencil;
       const double g = hp.A[0];
       bool ok = g != 0.0 && !stencil_stages && !hp.exact;
       for (int i = 1; i < d->stages; ++i) ok = ok && hp.A[i * mgb::MAX_ST + i] == g;
@@ -676,7 +764,11 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->dkind = dk;
   st->P = P; st->T = T; st->S = S;
   st->span = span;
-  const bool win_dedicated = dk == mgb::K_WIN && T <= 256 && span < 16 && n % 2 == 0;
+  // dedicated kernel: even n_x, <= 256 threads at 2 CTAs/SM; fixed-geometry builds
+  // (compile-time T, wrap replicas in the slice) for 16 x 256 and 16 x 512
+  const bool win_fixed = dk == mgb::K_WIN && P == 16 && (T == 256 || T == 512);
+  const bool win_dedicated = dk == mgb::K_WIN && P <= 16 && n % 2 == 0 && (T <= 256 || win_fixed);
+  if (win_fixed) st->S = hp.S = S = (T == 256 ? mgb::WinGeo<256>::S : mgb::WinGeo<512>::S);
   st->vec16 = win_dedicated;
   st->nst = dk == mgb::K_RK ? hp.stages + (hp.z_solve ? mgb::RK_ZSOLVE : 0) : 1;
   st->exact = (dk == mgb::K_WIN || dk == mgb::K_GEN) ? hp.exact : 1;
@@ -685,7 +777,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   if (dk == mgb::K_RK || dk == mgb::K_SLD) dbl += 4 * (size_t)mgb::scan_stride(T) + 4 * (size_t)T;
   if (dk == mgb::K_SLG) dbl += mgb::GmLayout::total(n);  // Hessenberg state, R, 2 TMA stages
   st->smem = (int)(sizeof(StepParams) + 8 * dbl);
-  if (win_dedicated)  // relax_win_kernel: double-buffered slice, weights in registers
+  if (win_dedicated)  // relax_win_kernel: double-buffered slice, weights as kernel parameters
     st->smem = (int)(8 * (2 * (size_t)P * S + 32));  // 2 slices + reduction
   // SL + GMRES on rows whose single-CTA slice + TMA stages exceed shared memory
   // (n_x > 8192): cluster kernels only
@@ -710,8 +802,9 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     auto it = registry().end();
     if (dk == mgb::K_SLG && T <= 256)  // register-rich variant (launch bound 256)
       it = registry().find(std::make_tuple(dk, P, span, 2, st->exact));
-    if (dk == mgb::K_WIN && !win_dedicated)  // wide slices / long stencils: generic-kernel variant
+    if (dk == mgb::K_WIN && !win_dedicated)  // odd n_x / 16384-point rows: generic-kernel variant
       it = registry().find(std::make_tuple(dk, P, span, 2, st->exact));
+    if (win_fixed) it = registry().find(std::make_tuple(dk, P, span, T == 512 ? 3 : 4, st->exact));
     if (it == registry().end()) it = registry().find(std::make_tuple(dk, P, span, st->nst, st->exact));
     if (it == registry().end()) { delete st; return fail(MGB_ERR_UNSUPPORTED, "no kernel instantiation for this layout"); }
     st->fn = it->second;
@@ -729,7 +822,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->max_grid = nb * sms;
   st->sms = sms;
   if (dk == mgb::K_SLG && T <= 256 && nb == 1) {
-    static const bool no_occ2 = std::getenv("MGB_SLG_NO_OCC2") != nullptr;
+    const bool no_occ2 = tuning().slg_no_occ2;
     const void* fn2 = nullptr;
     {
       std::lock_guard<std::mutex> lk(reg_mutex());
@@ -804,60 +897,56 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   L.a = *a;
   L.ws = nullptr;
   L.ws_slot = 0;
+  std::memcpy(L.win_w, st->hp.win_w, sizeof(L.win_w));
   long long grid = std::min<long long>(a->n_intervals, st->max_grid);
   // tooling / tests only: cap the grid so that every CTA walks a block of
   // several intervals (the chained head/tail hand-off of relax_win_kernel)
-  static const long long grid_cap = std::getenv("MGB_MAX_GRID") ? std::atoll(std::getenv("MGB_MAX_GRID")) : 0;
+  const long long grid_cap = tuning().max_grid;
   if (grid_cap > 0) grid = std::min(grid, grid_cap);
-  static const bool no_cluster = std::getenv("MGB_NO_CLUSTER") != nullptr;
-  static const bool cgs2 = std::getenv("MGB_CL_CGS2") != nullptr;
+  const Tuning& tn = tuning();
+  const bool no_cluster = tn.no_cluster, cgs2 = tn.cgs2;
   if (st->dkind == mgb::K_SLG && !no_cluster && !cgs2 && !st->clusters1.empty()) {
-    // fewest waves of clusters over the intervals; ties -> larger clusters
-    static const int force_c = std::getenv("MGB_C1_C") ? std::atoi(std::getenv("MGB_C1_C")) : 0;
+    // Launch plan over the level's intervals (each a chain of sequential GMRES
+    // solves, so a wave costs one chain whatever its width): the variant with
+    // the fewest waves of clusters; ties -> larger clusters.  When the last wave
+    // would be partial and a faster variant (one CTA/SM with every basis row
+    // resident, at least as large clusters) holds it in one wave of its own,
+    // that tail goes to the faster variant as a second launch.
+    auto usable = [&](const ClusterVariant& v) {
+      if (tn.c1_c && v.C != tn.c1_c) return false;
+      if (tn.c1_no_occ2 && v.occ == 2) return false;
+      // wide segments (cluster sizes 1-2 on 4096-point rows) measured slower than
+      // the single-CTA kernel for many-interval levels: opt-in only
+      if (v.P >= 4 && !tn.c1_wide && !tn.c1_c) return false;
+      return true;
+    };
     const ClusterVariant* best = nullptr;
     long long best_w = 0;
     for (const ClusterVariant& v : st->clusters1) {
-      if (force_c && v.C != force_c) continue;
-      static const bool no_occ2 = std::getenv("MGB_C1_NO_OCC2") != nullptr;
-      if (no_occ2 && v.occ == 2) continue;
-      // wide segments (cluster sizes 1-2 on 4096-point rows) measured slower than
-      // the single-CTA kernel for many-interval levels: opt-in only
-      static const bool wide = std::getenv("MGB_C1_WIDE") != nullptr;
-      if (v.P >= 4 && !wide && !force_c) continue;
+      if (!usable(v)) continue;
       const long long w = (a->n_intervals + v.max_clusters - 1) / v.max_clusters;
       if (!best || w < best_w) { best = &v; best_w = w; }
     }
-    // many-interval levels (> 2 cluster waves) run faster on the single-CTA kernel
-    static const long long max_waves1 = std::getenv("MGB_C1_WAVES")
-                                            ? std::atoll(std::getenv("MGB_C1_WAVES")) : 2;
-    if (best && (best_w <= max_waves1 || !st->fn)) {
-      const ClusterVariant& v = *best;
-      const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(ncl * v.C));
-      cfg.blockDim = dim3(v.T);
-      cfg.dynamicSmemBytes = v.smem;
-      cfg.stream = (cudaStream_t)stream;
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeClusterDimension;
-      attr.val.clusterDim.x = v.C;
-      attr.val.clusterDim.y = 1;
-      attr.val.clusterDim.z = 1;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      const StepParams* dpc = st->dp;
-      mgb::RelaxLaunch L1 = L;
-      L1.ws = v.ws;         // overflow basis rows (nullptr: all resident)
-      L1.ws_slot = v.K;     // resident row count
-      void* cargs[] = {(void*)&dpc, (void*)&L1};
-      CUDA_TRY(cudaLaunchKernelExC(&cfg, v.fn, cargs));
-      g_launches++;
-      return MGB_OK;
+    // many-interval levels (> max_waves cluster waves) run faster on the single-CTA kernel
+    if (best && (best_w <= tn.c1_waves || !st->fn)) {
+      long long head = a->n_intervals;
+      const ClusterVariant* tailv = nullptr;
+      if (best_w >= 2 && !tn.c1_no_split) {
+        const long long rem = a->n_intervals - (best_w - 1) * best->max_clusters;
+        for (const ClusterVariant& v : st->clusters1) {  // ordered by decreasing cluster size
+          if (!usable(v) || v.occ != 1 || v.ws || v.C < best->C || (v.C == best->C && best->occ == 1)) continue;
+          if (rem <= v.max_clusters) { tailv = &v; break; }
+        }
+        if (tailv) head = a->n_intervals - rem;
+      }
+      int rc = launch_cluster1(st, *best, sub_range(*a, 0, head, st->hp.n), stream);
+      if (rc == MGB_OK && tailv)
+        rc = launch_cluster1(st, *tailv, sub_range(*a, head, a->n_intervals - head, st->hp.n), stream);
+      return rc;
     }
   }
   if (st->dkind == mgb::K_SLG && !no_cluster) {
-    static const long long max_waves = std::getenv("MGB_CLUSTER_WAVES")
-                                           ? std::atoll(std::getenv("MGB_CLUSTER_WAVES")) : 2;
+    const long long max_waves = tn.cluster_waves;
     for (const ClusterVariant& v : st->clusters) {  // largest cluster size within max_waves
       if (a->n_intervals > max_waves * (long long)v.max_clusters) continue;
       const long long ncl = std::min<long long>(a->n_intervals, v.max_clusters);
