@@ -734,6 +734,10 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     if ((int)facs.size() > mgb::MAX_FAC) { delete st; return fail(MGB_ERR_UNSUPPORTED, "too many factors"); }
     hp.nfac = (int)facs.size();
     for (int f = 0; f < hp.nfac; ++f) fill_factor_tables(facs[f], T, P, hp.fac[f]);
+    if (tuning().debug)
+      for (int f = 0; f < hp.nfac; ++f)
+        fprintf(stderr, "[mgb] n=%d P=%d T=%d factor %d: a1=%.6g a2=%.6g dir=%d rho=%.4Lf win=%d\n", n, P, T, f,
+                hp.fac[f].a1, hp.fac[f].a2, hp.fac[f].dir, facs[f].rho, hp.fac[f].win);
     hp.gain_inv = (double)(1.0L / K);
     hp.shift = (int)mod_n(shift, n);
     if (hp.shift > n / 2) hp.shift -= n;

@@ -89,19 +89,23 @@ class DeviceProgram:
     gmres_cap: int = 20
     repeat: int = 1
     exact: bool = True
+    #: kind "callable": the user's ``Stepper(apply_fn=...)`` (stepping.py:276-295),
+    #: called with a CUDA tensor of shape (rows, n_x), returning the same
+    fn: Optional[object] = None
 
     def key(self):
         def b(a):
             return None if a is None else np.asarray(a).tobytes()
         return (self.kind, self.n_x, b(self.offsets), b(self.weights), b(self.offsets2),
                 b(self.weights2), b(self.rk_a), b(self.rk_b), self.implicit,
-                self.gmres_tol, self.gmres_cap, self.repeat, self.exact)
+                self.gmres_tol, self.gmres_cap, self.repeat, self.exact,
+                None if self.fn is None else id(self.fn))
 
     def repeated(self, times: int) -> "DeviceProgram":
         return DeviceProgram(self.kind, self.n_x, self.offsets, self.weights, self.offsets2,
                              self.weights2, self.rk_a, self.rk_b, self.implicit,
                              self.gmres_tol, self.gmres_cap, self.repeat * int(times),
-                             self.exact)
+                             self.exact, self.fn)
 
 
 _KIND = {"stencil": nat.MGB_STEP_STENCIL, "rk": nat.MGB_STEP_RK_STAGED,
@@ -196,6 +200,99 @@ class StepPlan:
                                       stream if stream is not None else stream_handle()))
 
 
+class _RawRows:
+    """Strided (rows, n_x) float64 view of raw device memory for torch
+    (``__cuda_array_interface__``; no copy)."""
+
+    def __init__(self, addr: int, rows: int, n_x: int, stride: int):
+        self.__cuda_array_interface__ = {
+            "shape": (rows, n_x), "typestr": "<f8", "data": (int(addr), False), "version": 3,
+            "strides": (8 * (int(stride) if rows > 1 else n_x), 8)}
+
+
+class CallablePlan:
+    """Interval relaxation around a user one-step callable
+    (``Stepper(apply_fn=...)``, stepping.py:276-295): the same pass semantics as
+    ``mgb_relax_args`` with every interval advanced at once by ONE call of the
+    callable on a ``(n_intervals, n_x)`` CUDA tensor per time step.  The
+    arithmetic of the step is the user's; the row updates, the residual and
+    the per-interval partial sums are torch device operations in the
+    reference's order (mgrit.py:132-166, 246)."""
+
+    threads = points_per_thread = smem = 0
+
+    def __init__(self, prog: DeviceProgram):
+        self._torch = require_cuda()
+        self.prog = prog
+
+    def reserve(self, stream=None) -> None:
+        pass
+
+    def _rows(self, addr, rows, stride):
+        t = self._torch
+        return t.as_tensor(_RawRows(addr, rows, self.prog.n_x, stride), device="cuda")
+
+    def _step(self, y):
+        for _ in range(max(1, int(self.prog.repeat))):
+            y = self.prog.fn(y)
+            if not (self._torch.is_tensor(y) and y.is_cuda and y.dtype == self._torch.float64):
+                raise TypeError("apply_fn must map a float64 CUDA tensor (rows, n_x) to the same; "
+                                "wrap numpy-only callables with stepping.host_callable")
+        return y
+
+    def relax(self, n_intervals: int, m: int, n_fsteps: int, *, k_global0: int = 0,
+              c_src=None, c_stride: int = 0, c_src0=None, e=None, e_stride: int = 0,
+              c_out=None, c_out_stride: int = 0, c_last_out=None, u=None, write_f: int = 0, g=None,
+              tail: int = 0, tail_out=None, tail_stride: int = 0, cref=None,
+              cref_stride: int = 0, cref_e=None, cref_e_stride: int = 0, partials=None,
+              stats_depth=None, stats_res=None, stream=None) -> None:
+        t = self._torch
+        nI, n = int(n_intervals), self.prog.n_x
+        if nI <= 0:
+            return
+        if c_src is not None:
+            y = self._rows(c_src, nI, c_stride).clone()
+        else:
+            y = t.zeros((nI, n), dtype=t.float64, device="cuda")
+        if c_src0 is not None and k_global0 == 0:
+            y[0] = self._rows(c_src0, 1, n)[0]
+        if e is not None:  # u[m::m] += e[1:] (mgrit.py:246): global intervals k >= 1
+            k0 = 1 if k_global0 == 0 else 0
+            if nI > k0:
+                y[k0:] += self._rows(e + 8 * k0 * e_stride, nI - k0, e_stride)
+        if c_out is not None:
+            self._rows(c_out, nI, c_out_stride).copy_(y)
+        for j in range(1, n_fsteps + 1):
+            y = self._step(y)
+            if g is not None:
+                y = y + self._rows(g + 8 * j * n, nI, m * n)
+            if write_f == 2 or (write_f == 1 and j == n_fsteps):
+                self._rows(u + 8 * j * n, nI, m * n).copy_(y)
+        if tail:
+            z = self._step(y)
+            if g is not None:
+                z = self._rows(g + 8 * m * n, nI, m * n) + z
+            if tail == 1:
+                self._rows(tail_out, nI, tail_stride).copy_(z)
+            else:
+                cr = self._rows(cref, nI, cref_stride)
+                if cref_e is not None:
+                    cr = cr + self._rows(cref_e, nI, cref_e_stride)
+                r = z - cr
+                if tail_out is not None:
+                    self._rows(tail_out, nI, tail_stride).copy_(r)
+                if partials is not None:
+                    t.as_tensor(_RawRows(partials, 1, nI, nI), device="cuda")[0].copy_((r * r).sum(dim=1))
+        if c_last_out is not None:
+            if c_src is not None:
+                last = self._rows(c_src + 8 * nI * c_stride, 1, n)[0].clone()
+            else:
+                last = t.zeros(n, dtype=t.float64, device="cuda")
+            if e is not None:
+                last += self._rows(e + 8 * nI * e_stride, 1, n)[0]
+            self._rows(c_last_out, 1, n)[0].copy_(last)
+
+
 def device_sum(partials, n: int, out, stream=None) -> None:
     nat.check(nat.load().mgb_sum(ctypes.c_void_p(partials), n, ctypes.c_void_p(out),
                                  stream if stream is not None else stream_handle()))
@@ -212,7 +309,7 @@ def plan_for(prog: DeviceProgram, tag=None) -> StepPlan:
     key = (torch.cuda.current_device(), tag, prog.key())
     plan = _PLAN_CACHE.get(key)
     if plan is None:
-        plan = StepPlan(prog)
+        plan = CallablePlan(prog) if prog.kind == "callable" else StepPlan(prog)
         _PLAN_CACHE[key] = plan
     return plan
 
