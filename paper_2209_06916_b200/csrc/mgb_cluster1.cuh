@@ -361,12 +361,14 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
     // re-orthogonalisation pass u_j - V a between the two barriers.
     double ai = 0.0, hn = 0.0, nu = 0.0;
     const uint32_t nthr = blockDim.x;
+    CL_TRS_INIT
     if (!c.vec) {
       const double tot = lane <= j + 1 ? c1_total(c, c.q, lane) : 0.0;
       ai = lane < j ? tot : 0.0;
       if (lane < j) coef[lane] = ai;
       __threadfence_block();
       asm volatile("bar.arrive 1, %0;" ::"r"(nthr) : "memory");
+      CL_TRS(10)
       nu = __shfl_sync(0xffffffffu, tot, j);
       const double cc = __shfl_sync(0xffffffffu, tot, (j + 1) & 31);
       const double na2 = c1_wsum(ai * ai);
@@ -388,12 +390,14 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
       }
       __threadfence_block();
       asm volatile("bar.arrive 2, %0;" ::"r"(nthr) : "memory");
+      CL_TRS(11)
     }
     c.q ^= 1;
     const double* Uh = c.U + pu * LD + c.HW;
     double v[KX];  // vector warps: u_j - V a on the segment +- 3r
     if (c.vec) {
       asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+      CL_TR(12)
       if (j < P.cap) {
 #pragma unroll
         for (int k = 0; k < KX; ++k) {
@@ -418,6 +422,7 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
           }
         }
       }
+      CL_TR(13)
       asm volatile("bar.sync 2, %0;" ::"r"(nthr) : "memory");
     }
     if (coef[CAP + 4] != 0.0) {  // zero right-hand side (circulant.py:274-278), uniform

@@ -32,7 +32,17 @@ __device__ unsigned long long g_cl_trace[16];
   }
 #define CL_TR_STEP \
   if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_cl_trace[15], 1ull);
+// second timer: first lane of the CTA's last warp (the cluster kernel's scalar warp)
+#define CL_TRS_INIT long long cl_s0_ = clock64();
+#define CL_TRS(k)                                                                     \
+  if (threadIdx.x == blockDim.x - 32 && blockIdx.x == 0) {                            \
+    const long long t_ = clock64();                                                   \
+    atomicAdd(&g_cl_trace[k], (unsigned long long)(t_ - cl_s0_));                    \
+    cl_s0_ = t_;                                                                      \
+  }
 #else
+#define CL_TRS_INIT
+#define CL_TRS(k)
 #define CL_TR_INIT
 #define CL_TR(k)
 #define CL_TR_STEP

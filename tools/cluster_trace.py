@@ -31,8 +31,9 @@ def timed(nm, fn, *a, **k):
             names = ["beta", "op2 stencil", "vi load+dot", "block_sum", "axpy+norm dot", "norm sum",
                      "V store+givens", "sync", "backsub+x", "row write+syncs", "", "", "", "", "", ""]
         elif mode == "c1":
-            names = ["scalars", "v_j", "Z_j", "u'", "Au'+dots", "syncthreads", "exchange",
-                     "backsub+x", "SL+b dots", "b exchange", "", "", "", "", "", ""]
+            names = ["wait bar2", "v_j", "Z_j", "u'", "Au'+dots", "syncthreads", "exchange",
+                     "backsub+x", "SL+b dots", "b exchange", "S:total+coef", "S:norm,sqrt,div",
+                     "wait bar1", "reorth pass", "", ""]
         else:
           names = ["beta+halo", "passA1", "passB1", "upd1+pub+pd2", "sum2", "corr+upd2+hn",
                  "V/Z+givens", "backsub+x", "SL apply", "row+barrier", "", "", "", "", "gmres total", "steps"]
