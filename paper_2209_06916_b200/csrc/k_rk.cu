@@ -15,7 +15,18 @@ namespace mgb {
   MGB_REG(K_RK, P, 0, 4 + RK_ZSOLVE, true); \
   MGB_REG(K_RK, P, 0, 5 + RK_ZSOLVE, true); \
   MGB_REG(K_RK, P, 0, 6 + RK_ZSOLVE, true);
+// dedicated SDIRK kernel (8 or 4 points per thread, all factors windowed, shift 0):
+// key span = 100 + 10 HL + HR (halo points of the -cL stencil), nst as above
+#define RKD_P(P, NS, HL, HR)                                                                   \
+  register_kernel(KernelKey{K_RK, P, 100 + 10 * HL + HR, NS, 1},                               \
+                  reinterpret_cast<const void*>(&relax_rkd_kernel<P, NS, false, HL, HR>));     \
+  register_kernel(KernelKey{K_RK, P, 100 + 10 * HL + HR, NS + RK_ZSOLVE, 1},                   \
+                  reinterpret_cast<const void*>(&relax_rkd_kernel<P, NS, true, HL, HR>));
+#define RKD(NS, HL, HR) RKD_P(8, NS, HL, HR) RKD_P(4, NS, HL, HR)
 void register_rk() {
+  RKD(1, 1, 0) RKD(2, 1, 0) RKD(3, 1, 0)
+  RKD(1, 2, 1) RKD(2, 2, 1) RKD(3, 2, 1)
+  RKD(1, 3, 2) RKD(2, 3, 2) RKD(3, 3, 2)
   RK_P(1)
   RK_P(2)
   RK_P(4)

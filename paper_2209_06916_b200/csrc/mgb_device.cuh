@@ -1281,6 +1281,299 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __r
 #endif
 }
 
+// x <- A^{-1} x when every factor of A is a windowed (fast-decaying) recurrence
+// and the symbol shift is zero: the windowed branch of chain_solve alone (same
+// operations in the same order, bitwise the same result), one CTA barrier per
+// factor; wb = 2 x 2T doubles of carry states, alternating per factor.
+template <int P>
+__device__ __forceinline__ void chain_solve_win(const StepParams& sp, double* wb0, int t, int T, bool own,
+                                                double (&x)[P]) {
+  const int nfac = sp.nfac;
+  for (int f = 0; f < nfac; ++f) {
+    const Factor& F = sp.fac[f];
+    const bool fwd = F.dir > 0;
+    const int tl = fwd ? t : T - 1 - t;
+    double* wb = wb0 + (f & 1) * 2 * T;
+    double s1 = 0.0, s2 = 0.0;
+    if (own) {
+      const double a1 = F.a1, a2 = F.a2;
+#pragma unroll
+      for (int qq = 0; qq < P; ++qq) {
+        const int q = fwd ? qq : P - 1 - qq;
+        const double yv = fma(a1, s1, fma(a2, s2, x[q]));
+        x[q] = yv;
+        s2 = s1;
+        s1 = yv;
+      }
+      wb[tl] = s1;
+      wb[T + tl] = s2;
+    }
+    __syncthreads();
+    if (own) {
+      double c1 = 0.0, c2 = 0.0;
+      const M2r M = ld_m2(F.M);
+      const int K = F.win;
+      int u = tl - K;
+      u += u < 0 ? T : 0;
+      double n1 = wb[u], n2 = wb[T + u];
+#pragma unroll 1
+      for (int k = K; k >= 1; --k) {
+        const double b1 = n1, b2 = n2;
+        if (k > 1) {
+          u = u + 1 == T ? 0 : u + 1;
+          n1 = wb[u];
+          n2 = wb[T + u];
+        }
+        mv2r(M, c1, c2);
+        c1 += b1;
+        c2 += b2;
+      }
+#pragma unroll
+      for (int qq = 0; qq < P; ++qq) {
+        const int q = fwd ? qq : P - 1 - qq;
+        x[q] = fma(F.h1[qq], c1, fma(F.h2[qq], c2, x[q]));
+      }
+    }
+  }
+  if (own) {
+    const double gi = sp.gain_inv;
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] *= gi;
+  }
+}
+
+// ------------------------------------------------ staged SDIRK relaxation
+// Dedicated kernel for implicit staged Runge-Kutta fine steps (SDIRK,
+// stepping.py:355-380) whose stage solves are all fast-decaying factors
+// (windowed carries) and whose -cL stencil is contiguous with span <= 6.
+// Differences from relax_kernel<K_RK>:
+//  * the stage values never round-trip through a resident row: the solved
+//    stage y_i stays in registers, only the HL + HR halo points a neighbour's
+//    stencil window needs are published to shared memory (3 of 8 for U3), so
+//    a stage costs one CTA barrier per factor plus one for the halo;
+//  * the Butcher sums are accumulated column-wise in the reference's order:
+//    after z_j every later right-hand side rhs_i (i > j) and the step result
+//    receive their a_ij z_j / b_j z_j term (rhs_i = x + a_i0 z_0 + a_i1 z_1 ...
+//    is formed in exactly that order, stepping.py:366-372, 378), the ones not
+//    needed next live in shared memory, so registers hold one stage at a time
+//    and the kernel fits two 512-thread CTAs per SM (<= 64 registers);
+//  * rows move between registers and HBM directly (16-byte accesses).
+constexpr int RKD_MAXH = 6;  // halo points (stencil span)
+
+#ifndef MGB_RKD_MINB
+#define MGB_RKD_MINB 2
+#endif
+template <int P, int NS, bool ZS, int HL, int HR>
+__global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const StepParams* __restrict__ gp,
+                                                           const RelaxLaunch L) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int SPB = (int)sizeof(StepParams);
+  {
+    const int4* src = reinterpret_cast<const int4*>(gp);
+    int4* dst = reinterpret_cast<int4*>(smem_raw);
+    for (int i = threadIdx.x; i < SPB / 16; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const StepParams& sp = *reinterpret_cast<const StepParams*>(smem_raw);
+  const mgb_relax_args& a = L.a;
+  const int T = sp.T, n = sp.n, t = threadIdx.x;
+  const bool own = t < T;
+  // shared layout (doubles): red[64] bc[8] | wb[2][2T] | edges[span][T] | acc[NS-1][P][T]
+  double* base = reinterpret_cast<double*>(smem_raw + SPB);
+  Ctx c;
+  c.sp = &sp;
+  c.n = n;
+  c.T = T;
+  c.S = sp.S;
+  c.t = t;
+  c.own = own;
+  c.row = nullptr;  // no resident row (shift == 0: checked by the host)
+  c.red = base;
+  c.bc = base + 64;
+  double* wb = base + 72;
+  c.scan = wb - 4 * scan_stride(T);  // chain_solve addresses the windowed buffers at scan + 4 SS
+  c.gm = nullptr;
+  c.ws = nullptr;
+  c.parity = 0;
+  c.phase = 0;
+  double* edges = wb + 4 * T;
+  // window of output q: own-chunk points q - HL .. q + HR (HL / HR halo points from
+  // chunk t-1 / t+1; the -cL stencil of upwind order p has HL = (p+1)/2, HR = (p-1)/2)
+  constexpr int span = HL + HR;
+  static_assert(span <= RKD_MAXH && HL <= P && HR <= P, "halo");
+  double* acc = edges + (size_t)span * T;
+  double wts[span + 1];
+#pragma unroll
+  for (int k = 0; k <= span; ++k) wts[k] = sp.win_w[k];
+  const int tl = t == 0 ? T - 1 : t - 1, tr = t == T - 1 ? 0 : t + 1;
+
+  for (long long k = blockIdx.x; k < a.n_intervals; k += gridDim.x) {
+    const long long kg = a.k_global0 + k;
+    const long long rowbase = k * (long long)a.m;
+    double y[P];
+    const double* csrc = (kg == 0 && a.c_src0) ? a.c_src0 : (a.c_src ? a.c_src + k * a.c_stride : nullptr);
+    if (own) {
+      if (csrc) {
+        load_chunk<P>(csrc, t, y);
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) y[q] = 0.0;
+      }
+      if (a.e && kg >= 1) {  // u[m::m] += e[1:] (mgrit.py:246)
+        double ev[P];
+        load_chunk<P>(a.e + k * a.e_stride, t, ev);
+#pragma unroll
+        for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], ev[q]);
+      }
+      if (a.c_out) store_chunk<P>(a.c_out + k * a.c_out_stride, t, y);
+    }
+    const int nsteps = a.n_fsteps + (a.tail ? 1 : 0);
+    for (int j = 1; j <= nsteps; ++j) {
+      const bool is_tail = j > a.n_fsteps;
+      for (int r = 0; r < sp.repeat; ++r) {
+        // ---- one SDIRK step y <- Phi y
+        double rhs[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) rhs[q] = y[q];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+          double r0[ZS ? P : 1];
+          if constexpr (ZS) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) r0[q] = rhs[q];
+          }
+          if (ZS && i > 0 && sp.nfac < 2) __syncthreads();  // previous solve's carry buffer is free
+          chain_solve_win<P>(sp, wb, t, T, own, rhs);  // rhs <- M^-1 rhs (one CTA barrier per factor)
+          double hl[HL > 0 ? HL : 1], hr[HR > 0 ? HR : 1];
+          if constexpr (!ZS) {
+            // publish the halo points: edges[h][t], h < HL: last HL points, then the first HR
+            if (own) {
+#pragma unroll
+              for (int h = 0; h < HL; ++h) edges[h * T + t] = rhs[P - HL + h];
+#pragma unroll
+              for (int h = 0; h < HR; ++h) edges[(HL + h) * T + t] = rhs[h];
+            }
+            __syncthreads();
+            if (own) {
+#pragma unroll
+              for (int h = 0; h < HL; ++h) hl[h] = edges[h * T + tl];
+#pragma unroll
+              for (int h = 0; h < HR; ++h) hr[h] = edges[(HL + h) * T + tr];
+            }
+          }
+          // ---- stage value z_q, then the column-wise Butcher accumulation (reference
+          // order, zero entries skipped): acc slot i2 - 2 holds rhs_{i2} for i2 >= i + 2,
+          // slot NS - 2 the step result; rhs_{i+1} (or the result after the last stage)
+          // goes to registers
+          double nxt[P];
+          if (own) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+              double zq;
+              if constexpr (ZS) {
+                // M y = rhs, M = I - gamma cL  =>  cL y = (y - rhs) / gamma (fast mode only)
+                zq = __dmul_rn(__dsub_rn(rhs[q], r0[q]), sp.inv_gamma);
+              } else {
+                // numpy's rolled sum (circulant.py:119-123): out = 0; out += w_k * roll(v)
+                zq = 0.0;
+#pragma unroll
+                for (int kk = 0; kk <= span; ++kk) {
+                  const int w = q + kk - HL;  // own-chunk index of the tap
+                  const double v = w < 0 ? hl[w + HL < 0 ? 0 : w + HL] : (w >= P ? hr[w - P < HR ? w - P : 0] : rhs[w]);
+                  zq = madd<true>(zq, wts[kk], v);
+                }
+              }
+#pragma unroll
+              for (int i2 = i + 1; i2 <= NS; ++i2) {
+                const double co = i2 < NS ? sp.A[i2 * MAX_ST + i] : sp.b[i];
+                double* slot = acc + (size_t)(i2 < NS ? i2 - 2 : NS - 2) * P * T;
+                const bool to_regs = (i2 == i + 1 && i2 < NS) || (i2 == NS && i == NS - 1);
+                const double b0 = i == 0 ? y[q] : slot[q * T + t];
+                const double v = co != 0.0 ? __dadd_rn(b0, __dmul_rn(co, zq)) : b0;
+                if (to_regs) nxt[q] = v; else slot[q * T + t] = v;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < P; ++q) rhs[q] = nxt[q];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) y[q] = rhs[q];  // the last column left the step result in rhs
+      }
+      const long long grow = is_tail ? rowbase + a.m : rowbase + j;
+      if (!is_tail) {
+        if (own) {
+          if (a.g) {
+            double gv[P];
+            load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+            for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], gv[q]);  // upd + g (mgrit.py:142)
+          }
+          if (a.write_f == 2 || (a.write_f == 1 && j == a.n_fsteps)) store_chunk<P>(a.u + grow * n, t, y);
+        }
+      } else if (a.tail == 1) {  // C-relaxation (mgrit.py:148-149)
+        if (own) {
+          if (a.g) {
+            double gv[P];
+            load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+            for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], gv[q]);
+          }
+          store_chunk<P>(a.tail_out + k * a.tail_stride, t, y);
+        }
+      } else {  // residual g + Phi u - u_C (mgrit.py:159-161)
+        double part = 0.0;
+        if (own) {
+          double rr[P];
+          if (a.g) {
+            double gv[P];
+            load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+            for (int q = 0; q < P; ++q) rr[q] = __dadd_rn(gv[q], y[q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) rr[q] = y[q];
+          }
+          double cr[P];
+          load_chunk<P>(a.cref + k * a.cref_stride, t, cr);
+          if (a.cref_e) {
+            double ev[P];
+            load_chunk<P>(a.cref_e + k * a.cref_e_stride, t, ev);
+#pragma unroll
+            for (int q = 0; q < P; ++q) cr[q] = __dadd_rn(cr[q], ev[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            rr[q] = __dsub_rn(rr[q], cr[q]);
+            part = fma(rr[q], rr[q], part);
+          }
+          if (a.tail_out) store_chunk<P>(a.tail_out + k * a.tail_stride, t, rr);
+        }
+        if (a.partials) {
+          const double sum = block_sum(c, part);
+          if (t == 0) a.partials[k] = sum;
+        }
+      }
+    }
+    if (a.c_last_out && k == a.n_intervals - 1 && own) {  // final C-point (k+1 >= 1)
+      double cl[P];
+      if (a.c_src) {
+        load_chunk<P>(a.c_src + (k + 1) * a.c_stride, t, cl);
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) cl[q] = 0.0;
+      }
+      if (a.e) {
+        double ev[P];
+        load_chunk<P>(a.e + (k + 1) * a.e_stride, t, ev);
+#pragma unroll
+        for (int q = 0; q < P; ++q) cl[q] = __dadd_rn(cl[q], ev[q]);
+      }
+      store_chunk<P>(a.c_last_out, t, cl);
+    }
+  }
+}
+
 // ------------------------------------------- explicit-stencil relaxation
 // Dedicated kernel for assembled explicit stencils (the fine ERK levels):
 // stencil weights are kernel parameters (constant-bank operands, no registers),

@@ -31,6 +31,49 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+// Launch choices are plan-time parameters with the defaults below.  The MGB_*
+// environment variables override them for tooling only (variant sweeps,
+// bisection, the chained-interval tests); they are read once per process.
+struct Tuning {
+  bool debug = false;
+  bool no_cluster = false;    // MGB_NO_CLUSTER: single-CTA GMRES on every level
+  bool cgs2 = false;          // MGB_CL_CGS2: previous two-reduction cluster kernel
+  int c1_c = 0;               // MGB_C1_C: force one cluster size
+  bool c1_no_occ2 = false;    // MGB_C1_NO_OCC2: no 2-CTA/SM cluster builds
+  bool c1_wide = false;       // MGB_C1_WIDE: allow wide-segment cluster builds
+  bool c1_no_split = false;   // MGB_C1_NO_SPLIT: no second launch for a partial last wave
+  long long c1_waves = 2;     // MGB_C1_WAVES: cluster waves beyond which the single-CTA kernel runs
+  long long cluster_waves = 2;  // MGB_CLUSTER_WAVES: same for the two-reduction kernel
+  int c1_segk = 1;            // MGB_C1_SEGK: smallest segment width considered
+  bool slg_no_occ2 = false;   // MGB_SLG_NO_OCC2: no 2-CTA/SM single-CTA GMRES build
+  bool rk_stencil = false;    // MGB_RK_STENCIL: SDIRK stage values by the stencil in fast mode too
+  bool no_rkd = false;        // MGB_NO_RKD: staged SDIRK on the generic kernel
+  long long max_grid = 0;     // MGB_MAX_GRID: cap the grid (tests: many intervals per CTA)
+};
+const Tuning& tuning() {
+  static const Tuning t = [] {
+    Tuning x;
+    auto flag = [](const char* k) { return std::getenv(k) != nullptr; };
+    auto num = [](const char* k, long long d) { const char* v = std::getenv(k); return v ? std::atoll(v) : d; };
+    x.debug = flag("MGB_DEBUG");
+    x.no_cluster = flag("MGB_NO_CLUSTER");
+    x.cgs2 = flag("MGB_CL_CGS2");
+    x.c1_c = (int)num("MGB_C1_C", 0);
+    x.c1_no_occ2 = flag("MGB_C1_NO_OCC2");
+    x.c1_wide = flag("MGB_C1_WIDE");
+    x.c1_no_split = flag("MGB_C1_NO_SPLIT");
+    x.c1_waves = num("MGB_C1_WAVES", 2);
+    x.cluster_waves = num("MGB_CLUSTER_WAVES", 2);
+    x.c1_segk = (int)num("MGB_C1_SEGK", 1);
+    x.slg_no_occ2 = flag("MGB_SLG_NO_OCC2");
+    x.rk_stencil = flag("MGB_RK_STENCIL");
+    x.no_rkd = flag("MGB_NO_RKD");
+    x.max_grid = num("MGB_MAX_GRID", 0);
+    return x;
+  }();
+  return t;
+}
+
 #define CUDA_TRY(expr)                                                           \
   do {                                                                           \
     cudaError_t e_ = (expr);                                                     \
@@ -377,47 +420,6 @@ struct mgb_step {
 };
 
 namespace {
-// Launch choices are plan-time parameters with the defaults below.  The MGB_*
-// environment variables override them for tooling only (variant sweeps,
-// bisection, the chained-interval tests); they are read once per process.
-struct Tuning {
-  bool debug = false;
-  bool no_cluster = false;    // MGB_NO_CLUSTER: single-CTA GMRES on every level
-  bool cgs2 = false;          // MGB_CL_CGS2: previous two-reduction cluster kernel
-  int c1_c = 0;               // MGB_C1_C: force one cluster size
-  bool c1_no_occ2 = false;    // MGB_C1_NO_OCC2: no 2-CTA/SM cluster builds
-  bool c1_wide = false;       // MGB_C1_WIDE: allow wide-segment cluster builds
-  bool c1_no_split = false;   // MGB_C1_NO_SPLIT: no second launch for a partial last wave
-  long long c1_waves = 2;     // MGB_C1_WAVES: cluster waves beyond which the single-CTA kernel runs
-  long long cluster_waves = 2;  // MGB_CLUSTER_WAVES: same for the two-reduction kernel
-  int c1_segk = 1;            // MGB_C1_SEGK: smallest segment width considered
-  bool slg_no_occ2 = false;   // MGB_SLG_NO_OCC2: no 2-CTA/SM single-CTA GMRES build
-  bool rk_stencil = false;    // MGB_RK_STENCIL: SDIRK stage values by the stencil in fast mode too
-  long long max_grid = 0;     // MGB_MAX_GRID: cap the grid (tests: many intervals per CTA)
-};
-const Tuning& tuning() {
-  static const Tuning t = [] {
-    Tuning x;
-    auto flag = [](const char* k) { return std::getenv(k) != nullptr; };
-    auto num = [](const char* k, long long d) { const char* v = std::getenv(k); return v ? std::atoll(v) : d; };
-    x.debug = flag("MGB_DEBUG");
-    x.no_cluster = flag("MGB_NO_CLUSTER");
-    x.cgs2 = flag("MGB_CL_CGS2");
-    x.c1_c = (int)num("MGB_C1_C", 0);
-    x.c1_no_occ2 = flag("MGB_C1_NO_OCC2");
-    x.c1_wide = flag("MGB_C1_WIDE");
-    x.c1_no_split = flag("MGB_C1_NO_SPLIT");
-    x.c1_waves = num("MGB_C1_WAVES", 2);
-    x.cluster_waves = num("MGB_CLUSTER_WAVES", 2);
-    x.c1_segk = (int)num("MGB_C1_SEGK", 1);
-    x.slg_no_occ2 = flag("MGB_SLG_NO_OCC2");
-    x.rk_stencil = flag("MGB_RK_STENCIL");
-    x.max_grid = num("MGB_MAX_GRID", 0);
-    return x;
-  }();
-  return t;
-}
-
 // Arguments of the sub-pass over intervals [k0, k0 + cnt) of pass ``a``.
 mgb_relax_args sub_range(const mgb_relax_args& a, long long k0, long long cnt, int n) {
   mgb_relax_args s = a;
@@ -660,6 +662,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     default: delete st; return fail(MGB_ERR_INVALID, "unknown step kind");
   }
   int P, T, S;
+  long long rk_front = 1;  // first offset of a contiguous -cL stencil (RK kind)
   int rc = choose_layout(dk, n, P, T, S);
   if (rc) { delete st; return rc; }
   hp.n = n; hp.P = P; hp.T = T; hp.S = S;
@@ -710,6 +713,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     bool inc = true;
     for (int k = 1; k < d->n_taps; ++k) inc = inc && off[k] > off[k - 1];
     const long long sp1 = off.back() - off.front();
+    rk_front = inc ? off.front() : 1;
     if (inc && sp1 <= 6 && T >= 8) {
       hp.win1_ok = 1;
       hp.win_lo = (int)mod_n(off.front(), n);
@@ -783,6 +787,20 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
   st->smem = (int)(sizeof(StepParams) + 8 * dbl);
   if (win_dedicated)  // relax_win_kernel: double-buffered slice, weights as kernel parameters
     st->smem = (int)(8 * (2 * (size_t)P * S + 32));  // 2 slices + reduction
+  // dedicated SDIRK kernel: 8 (or 4) points per thread, every factor a windowed (fast-decaying)
+  // recurrence, no symbol shift, -cL stencil with (HL, HR) halo of upwind order 1 / 3 / 5
+  int rkd_key = 0;
+  if (dk == mgb::K_RK && hp.implicit && (P == 8 || P == 4) && hp.shift == 0 && hp.win1_ok && hp.stages <= 3 &&
+      !tuning().no_rkd) {
+    bool allwin = hp.nfac >= 1;
+    for (int f = 0; f < hp.nfac; ++f) allwin = allwin && hp.fac[f].win > 0;
+    const int HL = (int)-rk_front, HR = hp.win_span - HL;
+    if (allwin && ((HL == 1 && HR == 0) || (HL == 2 && HR == 1) || (HL == 3 && HR == 2)))
+      rkd_key = 100 + 10 * HL + HR;
+  }
+  if (rkd_key)
+    st->smem = (int)(sizeof(StepParams) +
+                     8 * (72 + 4 * (size_t)T + (size_t)hp.win_span * T + (size_t)(hp.stages - 1) * P * T));
   // SL + GMRES on rows whose single-CTA slice + TMA stages exceed shared memory
   // (n_x > 8192): cluster kernels only
   const bool cluster_only = dk == mgb::K_SLG && st->smem > 227 * 1024;
@@ -809,6 +827,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     if (dk == mgb::K_WIN && !win_dedicated)  // odd n_x / 16384-point rows: generic-kernel variant
       it = registry().find(std::make_tuple(dk, P, span, 2, st->exact));
     if (win_fixed) it = registry().find(std::make_tuple(dk, P, span, T == 512 ? 3 : 4, st->exact));
+    if (rkd_key) it = registry().find(std::make_tuple(dk, P, rkd_key, st->nst, st->exact));
     if (it == registry().end()) it = registry().find(std::make_tuple(dk, P, span, st->nst, st->exact));
     if (it == registry().end()) { delete st; return fail(MGB_ERR_UNSUPPORTED, "no kernel instantiation for this layout"); }
     st->fn = it->second;
