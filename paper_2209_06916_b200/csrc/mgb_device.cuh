@@ -92,6 +92,23 @@ struct StepParams {
 };
 static_assert(sizeof(StepParams) % 16 == 0, "StepParams must be 16-byte sized");
 
+// Constants of the dedicated SDIRK kernel (relax_rkd_kernel), passed as kernel
+// parameters: the parameter space is a constant bank, so factor coefficients,
+// carry responses and tableau entries are instruction operands (no shared-memory
+// loads, no registers).
+constexpr int RKD_MAXF = 3;   // factors of the stage operator
+constexpr int RKD_MAXP = 8;   // points per thread
+constexpr int RKD_KMAX = 16;  // longest carry window (chunks)
+struct RkdFactor {
+  double a1, a2, M[4], h1[RKD_MAXP], h2[RKD_MAXP];
+  int dir, win;
+};
+struct RkdConst {
+  RkdFactor f[RKD_MAXF];
+  double A[9], b[3], gain_inv, inv_gamma;
+  int nfac, pad_;
+};
+
 struct RelaxLaunch {
   mgb_relax_args a;
   double* ws;            // GMRES workspace base (slot = blockIdx.x)
@@ -99,6 +116,7 @@ struct RelaxLaunch {
   // register-window stencil weights (relax_win_kernel): kernel parameters live in
   // the constant bank, so every tap weight is an instruction operand, not a register
   double win_w[32];
+  RkdConst rk;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -1284,61 +1302,66 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __r
 // x <- A^{-1} x when every factor of A is a windowed (fast-decaying) recurrence
 // and the symbol shift is zero: the windowed branch of chain_solve alone (same
 // operations in the same order, bitwise the same result), one CTA barrier per
-// factor; wb = 2 x 2T doubles of carry states, alternating per factor.
-template <int P>
-__device__ __forceinline__ void chain_solve_win(const StepParams& sp, double* wb0, int t, int T, bool own,
-                                                double (&x)[P]) {
-  const int nfac = sp.nfac;
-  for (int f = 0; f < nfac; ++f) {
-    const Factor& F = sp.fac[f];
-    const bool fwd = F.dir > 0;
-    const int tl = fwd ? t : T - 1 - t;
-    double* wb = wb0 + (f & 1) * 2 * T;
+// factor.  Carry states are stored as (s1, s2) pairs at index chunk + RKD_KMAX
+// with the last RKD_KMAX chunks replicated in front (the periodic wrap), so the
+// look-back reads K consecutive 16-byte words; wb0 = 2 buffers of
+// (T + RKD_KMAX) pairs, alternating per factor.
+template <int P, bool FWD>
+__device__ __forceinline__ void rkd_factor(const RkdFactor& F, double2* wb, int t, int T, bool own,
+                                           double (&x)[P]) {
+  const int tl = FWD ? t : T - 1 - t;
+  if (own) {
     double s1 = 0.0, s2 = 0.0;
-    if (own) {
-      const double a1 = F.a1, a2 = F.a2;
 #pragma unroll
-      for (int qq = 0; qq < P; ++qq) {
-        const int q = fwd ? qq : P - 1 - qq;
-        const double yv = fma(a1, s1, fma(a2, s2, x[q]));
-        x[q] = yv;
-        s2 = s1;
-        s1 = yv;
-      }
-      wb[tl] = s1;
-      wb[T + tl] = s2;
+    for (int qq = 0; qq < P; ++qq) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int q = FWD ? qq : P - 1 - qq;
+      const double yv = fma(F.a1, s1, fma(F.a2, s2, x[q]));
+      x[q] = yv;
+      s2 = s1;
+      s1 = yv;
     }
-    __syncthreads();
-    if (own) {
-      double c1 = 0.0, c2 = 0.0;
-      const M2r M = ld_m2(F.M);
-      const int K = F.win;
-      int u = tl - K;
-      u += u < 0 ? T : 0;
-      double n1 = wb[u], n2 = wb[T + u];
-#pragma unroll 1
-      for (int k = K; k >= 1; --k) {
-        const double b1 = n1, b2 = n2;
-        if (k > 1) {
-          u = u + 1 == T ? 0 : u + 1;
-          n1 = wb[u];
-          n2 = wb[T + u];
-        }
-        mv2r(M, c1, c2);
-        c1 += b1;
-        c2 += b2;
-      }
+    wb[tl + RKD_KMAX] = make_double2(s1, s2);
+    if (tl >= T - RKD_KMAX) wb[tl + RKD_KMAX - T] = make_double2(s1, s2);
+  }
+  __syncthreads();
+  if (own) {
+    double c1 = 0.0, c2 = 0.0;
+    const int K = F.win;
+    const double2* p = wb + tl + RKD_KMAX - K;  // chunks tl - K .. tl - 1
+#pragma unroll 2
+    for (int k = 0; k < K; ++k) {
+      const double2 bb = p[k];
+      const double n1 = fma(F.M[0], c1, F.M[1] * c2);
+      const double n2 = fma(F.M[2], c1, F.M[3] * c2);
+      c1 = n1 + bb.x;
+      c2 = n2 + bb.y;
+    }
 #pragma unroll
-      for (int qq = 0; qq < P; ++qq) {
-        const int q = fwd ? qq : P - 1 - qq;
-        x[q] = fma(F.h1[qq], c1, fma(F.h2[qq], c2, x[q]));
-      }
+    for (int qq = 0; qq < P; ++qq) {
+      const int q = FWD ? qq : P - 1 - qq;
+      x[q] = fma(F.h1[qq], c1, fma(F.h2[qq], c2, x[q]));
+    }
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void chain_solve_win(const RkdConst& rk, double2* wb0, int t, int T, bool own,
+                                                double (&x)[P]) {
+#pragma unroll
+  for (int f = 0; f < RKD_MAXF; ++f) {
+    if (f < rk.nfac) {
+      double2* wb = wb0 + (f & 1) * (T + RKD_KMAX);
+      if (rk.f[f].dir > 0)
+        rkd_factor<P, true>(rk.f[f], wb, t, T, own, x);
+      else
+        rkd_factor<P, false>(rk.f[f], wb, t, T, own, x);
     }
   }
   if (own) {
-    const double gi = sp.gain_inv;
 #pragma unroll
-    for (int q = 0; q < P; ++q) x[q] *= gi;
+    for (int q = 0; q < P; ++q) x[q] *= rk.gain_inv;
   }
 }
 
@@ -1378,7 +1401,7 @@ __global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const Step
   const mgb_relax_args& a = L.a;
   const int T = sp.T, n = sp.n, t = threadIdx.x;
   const bool own = t < T;
-  // shared layout (doubles): red[64] bc[8] | wb[2][2T] | edges[span][T] | acc[NS-1][P][T]
+  // shared layout (doubles): red[64] bc[8] | wb[2][T + RKD_KMAX] pairs | edges[span][T] | acc[NS-1][P][T]
   double* base = reinterpret_cast<double*>(smem_raw + SPB);
   Ctx c;
   c.sp = &sp;
@@ -1390,13 +1413,14 @@ __global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const Step
   c.row = nullptr;  // no resident row (shift == 0: checked by the host)
   c.red = base;
   c.bc = base + 64;
-  double* wb = base + 72;
-  c.scan = wb - 4 * scan_stride(T);  // chain_solve addresses the windowed buffers at scan + 4 SS
+  double2* wb = reinterpret_cast<double2*>(base + 72);
+  c.scan = nullptr;
   c.gm = nullptr;
   c.ws = nullptr;
   c.parity = 0;
   c.phase = 0;
-  double* edges = wb + 4 * T;
+  double* edges = base + 72 + 4 * (T + RKD_KMAX);
+  const RkdConst& rk = L.rk;
   // window of output q: own-chunk points q - HL .. q + HR (HL / HR halo points from
   // chunk t-1 / t+1; the -cL stencil of upwind order p has HL = (p+1)/2, HR = (p-1)/2)
   constexpr int span = HL + HR;
@@ -1442,8 +1466,8 @@ __global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const Step
 #pragma unroll
             for (int q = 0; q < P; ++q) r0[q] = rhs[q];
           }
-          if (ZS && i > 0 && sp.nfac < 2) __syncthreads();  // previous solve's carry buffer is free
-          chain_solve_win<P>(sp, wb, t, T, own, rhs);  // rhs <- M^-1 rhs (one CTA barrier per factor)
+          if (ZS && i > 0 && rk.nfac < 2) __syncthreads();  // previous solve's carry buffer is free
+          chain_solve_win<P>(rk, wb, t, T, own, rhs);  // rhs <- M^-1 rhs (one CTA barrier per factor)
           double hl[HL > 0 ? HL : 1], hr[HR > 0 ? HR : 1];
           if constexpr (!ZS) {
             // publish the halo points: edges[h][t], h < HL: last HL points, then the first HR
@@ -1472,7 +1496,7 @@ __global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const Step
               double zq;
               if constexpr (ZS) {
                 // M y = rhs, M = I - gamma cL  =>  cL y = (y - rhs) / gamma (fast mode only)
-                zq = __dmul_rn(__dsub_rn(rhs[q], r0[q]), sp.inv_gamma);
+                zq = __dmul_rn(__dsub_rn(rhs[q], r0[q]), rk.inv_gamma);
               } else {
                 // numpy's rolled sum (circulant.py:119-123): out = 0; out += w_k * roll(v)
                 zq = 0.0;
@@ -1485,7 +1509,7 @@ __global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const Step
               }
 #pragma unroll
               for (int i2 = i + 1; i2 <= NS; ++i2) {
-                const double co = i2 < NS ? sp.A[i2 * MAX_ST + i] : sp.b[i];
+                const double co = i2 < NS ? rk.A[i2 * 3 + i] : rk.b[i];
                 double* slot = acc + (size_t)(i2 < NS ? i2 - 2 : NS - 2) * P * T;
                 const bool to_regs = (i2 == i + 1 && i2 < NS) || (i2 == NS && i == NS - 1);
                 const double b0 = i == 0 ? y[q] : slot[q * T + t];

@@ -407,6 +407,7 @@ struct mgb_step {
   StepParams* dp = nullptr;
   int dkind = 0, P = 1, T = 1, S = 1, span = 0, nst = 1, exact = 1;
   bool vec16 = false;  // relax_win_kernel: 16-byte row accesses
+  mgb::RkdConst rk = {};  // relax_rkd_kernel constants
   int threads = 32, smem = 0, max_grid = 1, sms = 148;
   const void* fn = nullptr;
   // SL_GMRES single-CTA: 2 CTAs/SM variant for levels that need > 1 wave of fn
@@ -516,6 +517,8 @@ void prepare_clusters1(mgb_step* st) {
     if (n % C) continue;
     const int nc = n / C;
     int segk = 0, NW = 0, nwmax = 0;
+    // (points per lane, vector-warp bound); 16 warps of 32-point segments measured
+    // slower than 8 warps of 64 (cfg4 L3: 65.2 vs 63.8 ms)
     const int cand[6][2] = {{1, 8}, {2, 8}, {2, 16}, {4, 16}, {8, 8}, {8, 16}};
     const int min_segk = tuning().c1_segk;
     for (const auto& cd : cand) {
@@ -795,12 +798,30 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     bool allwin = hp.nfac >= 1;
     for (int f = 0; f < hp.nfac; ++f) allwin = allwin && hp.fac[f].win > 0;
     const int HL = (int)-rk_front, HR = hp.win_span - HL;
+    allwin = allwin && hp.nfac <= mgb::RKD_MAXF;
     if (allwin && ((HL == 1 && HR == 0) || (HL == 2 && HR == 1) || (HL == 3 && HR == 2)))
       rkd_key = 100 + 10 * HL + HR;
   }
-  if (rkd_key)
-    st->smem = (int)(sizeof(StepParams) +
-                     8 * (72 + 4 * (size_t)T + (size_t)hp.win_span * T + (size_t)(hp.stages - 1) * P * T));
+  if (rkd_key) {
+    st->smem = (int)(sizeof(StepParams) + 8 * (72 + 4 * (size_t)(T + mgb::RKD_KMAX) + (size_t)hp.win_span * T +
+                                               (size_t)(hp.stages - 1) * P * T));
+    mgb::RkdConst& rk = st->rk;
+    std::memset(&rk, 0, sizeof(rk));
+    rk.nfac = hp.nfac;
+    for (int f = 0; f < hp.nfac; ++f) {
+      const Factor& F = hp.fac[f];
+      mgb::RkdFactor& R = rk.f[f];
+      R.a1 = F.a1; R.a2 = F.a2; R.dir = F.dir; R.win = F.win;
+      for (int k = 0; k < 4; ++k) R.M[k] = F.M[k];
+      for (int q = 0; q < P; ++q) { R.h1[q] = F.h1[q]; R.h2[q] = F.h2[q]; }
+    }
+    for (int i = 0; i < hp.stages; ++i) {
+      rk.b[i] = hp.b[i];
+      for (int j = 0; j < hp.stages; ++j) rk.A[i * 3 + j] = hp.A[i * mgb::MAX_ST + j];
+    }
+    rk.gain_inv = hp.gain_inv;
+    rk.inv_gamma = hp.inv_gamma;
+  }
   // SL + GMRES on rows whose single-CTA slice + TMA stages exceed shared memory
   // (n_x > 8192): cluster kernels only
   const bool cluster_only = dk == mgb::K_SLG && st->smem > 227 * 1024;
@@ -921,6 +942,7 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   L.ws = nullptr;
   L.ws_slot = 0;
   std::memcpy(L.win_w, st->hp.win_w, sizeof(L.win_w));
+  L.rk = st->rk;
   long long grid = std::min<long long>(a->n_intervals, st->max_grid);
   // tooling / tests only: cap the grid so that every CTA walks a block of
   // several intervals (the chained head/tail hand-off of relax_win_kernel)
@@ -931,7 +953,9 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   if (st->dkind == mgb::K_SLG && !no_cluster && !cgs2 && !st->clusters1.empty()) {
     // Launch plan over the level's intervals (each a chain of sequential GMRES
     // solves, so a wave costs one chain whatever its width): the variant with
-    // the fewest waves of clusters; ties -> larger clusters.  When the last wave
+    // the fewest waves of clusters; ties -> larger clusters, except that a 2-CTA/SM build
+    // whose basis overflows to the workspace yields to a one-CTA/SM build with every row
+    // resident (cfg4 L2: 162 -> 150 ms; cfg2 L2 keeps its resident 2-CTA/SM build).  When the last wave
     // would be partial and a faster variant (one CTA/SM with every basis row
     // resident, at least as large clusters) holds it in one wave of its own,
     // that tail goes to the faster variant as a second launch.
@@ -948,7 +972,7 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
     for (const ClusterVariant& v : st->clusters1) {
       if (!usable(v)) continue;
       const long long w = (a->n_intervals + v.max_clusters - 1) / v.max_clusters;
-      if (!best || w < best_w) { best = &v; best_w = w; }
+      if (!best || w < best_w || (w == best_w && best->occ == 2 && best->ws && v.occ == 1 && !v.ws)) { best = &v; best_w = w; }
     }
     // many-interval levels (> max_waves cluster waves) run faster on the single-CTA kernel
     if (best && (best_w <= tn.c1_waves || !st->fn)) {
