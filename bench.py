@@ -155,10 +155,22 @@ def pass_work(cf, level, n_int, m, prog, kind):
       CF: m steps (m-1 F + the residual tail): reads the C-point and correction
           rows once, writes every F/C row once (fine level: the iterate).
     flops = 2 * taps per point-step (one multiply + one add per tap)."""
-    if prog.kind != "stencil":
-        return None, None
     n, taps = cf.n_x, len(prog.offsets)
-    flops = 2.0 * taps * n * n_int * m
+    if prog.kind == "rk":
+        # staged RK (stepping.py:355-380) per point-step: per stage one -cL stencil
+        # (2 * taps) and, for SDIRK, one stage solve with the factorised operator
+        # (4 flops per root of its symbol: recurrence + carry response, + 1 gain);
+        # plus 2 flops per non-zero tableau entry (the Butcher sums)
+        A, b = np.asarray(prog.rk_a), np.asarray(prog.rk_b)
+        ns = len(b)
+        solve = (4.0 * (len(prog.offsets2) - 1) + 1.0) if prog.implicit else 0.0
+        butcher = 2.0 * (np.count_nonzero(np.tril(A.reshape(ns, ns), -1)) + np.count_nonzero(b))
+        per_pt = ns * (2.0 * taps + solve) + butcher
+    elif prog.kind == "stencil":
+        per_pt = 2.0 * taps
+    else:
+        return None, None
+    flops = per_pt * n * n_int * m
     rows = {"FC": 2 * n_int, "FR": 3 * n_int, "CF": n_int * m + 1 + 2 * (n_int + 1)}[kind]
     return flops, 8.0 * n * rows
 
@@ -191,7 +203,9 @@ def rooflines(cf, prob, passes, total_ms, n_int0, fp64_peak):
             continue
         cnt, ms = passes[name]
         t = ms / cnt / 1e3
-        issue = fp64_peak * (0.5 if prog.exact else 1.0)
+        # exact explicit stencils issue DMUL + DADD per tap; staged RK mixes fused solves
+        # with exact stencil / tableau sums and is reported against the DFMA peak
+        issue = fp64_peak * (0.5 if (prog.exact and prog.kind == "stencil") else 1.0)
         fp64_bound = flops / (issue * 1e9) >= nbytes / (hbm_peak * 1e9)
         traffic, tsrc = traffic_of(cf.name, name)
         if fp64_bound:

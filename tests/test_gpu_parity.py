@@ -264,7 +264,8 @@ _FULL = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full
 # config's level structure on a smaller grid (tests/golden/make_full.py)
 _CASES = {"cfg1": ("cfg1", None, None), "cfg2": ("cfg2", None, None),
           "cfg3": ("cfg3", None, None), "cfg4": ("cfg4", None, None),
-          "cfg4p": ("cfg4", 1024, 65536), "cfg5p": ("cfg5", 16384, 16384)}
+          "cfg4p": ("cfg4", 1024, 65536), "cfg5p": ("cfg5", 16384, 16384),
+          "cfg5q": ("cfg5", 16384, 131072)}
 # reduction-order self-noise of the reference measured on reduced grids (SURVEY
 # 0.6 / 8c), used when a case has no full-size calibration run
 _REDUCED_ENVELOPE = {3: 1.1e-11, 5: 2.9e-8}
