@@ -1714,7 +1714,7 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_win_kernel(const StepParams*
 #pragma unroll
   for (int k = 0; k <= SPAN; ++k) wd[k] = L.win_w[k];
   const int t = threadIdx.x;
-  const bool own = t < T;
+  const bool own = TT > 0 ? true : t < T;  // fixed geometry: one chunk per thread
   const int lo = gp->win_lo;
   int tb = t + lo / P;
   tb = tb >= T ? tb - T : tb;

@@ -56,7 +56,13 @@ def test_shift_and_identity(n):
 
 @pytest.mark.parametrize("p,c,n,nt,m", [(1, 0.85, 1024, 1024, 8), (3, 0.85, 4096, 256, 8),
                                         (5, 0.85, 512, 256, 16), (3, 1.382, 64, 64, 4),
-                                        (3, 0.85, 16384, 64, 8)])
+                                        (3, 0.85, 16384, 64, 8),
+                                        # fixed-geometry builds of the explicit kernel: 16 x 256
+                                        # and 16 x 512 threads, 31-tap ERK5 stencils, many
+                                        # intervals per CTA (4096 x 4096: 512 intervals / 296 CTAs)
+                                        (5, 0.85, 4096, 64, 16), (5, 0.85, 8192, 64, 16),
+                                        (3, 0.85, 8192, 64, 8), (1, 0.85, 8192, 32, 8),
+                                        (3, 0.85, 4096, 4096, 8)])
 def test_f_relax_bitwise(p, c, n, nt, m):
     spec = P.DiscretizationSpec("erk", p, c, n, nt)
     st = P.mol_stepper(spec)
