@@ -23,3 +23,12 @@ for pass in $passes; do
   python tools/ncu_inst_summary.py gpurun_out/${tag}_source.csv 25 > gpurun_out/${tag}_source_inst.txt 2>&1
   rm -f gpurun_out/${tag}_source.csv
 done
+# extra captures of the other configs' fine passes + the parity report
+for cp in cfg2:L0.CF cfg3:L0.FC; do
+  c=${cp%%:*}; pass=${cp##*:}; tag=${c}_$(echo $pass | tr -d .)
+  timeout 900 bash tools/ncu_pass.sh $c $pass $tag
+  python tools/ncu_src_summary.py gpurun_out/${tag}_source.csv 25 > gpurun_out/${tag}_source_stalls.txt 2>&1
+  python tools/ncu_inst_summary.py gpurun_out/${tag}_source.csv 25 > gpurun_out/${tag}_source_inst.txt 2>&1
+  rm -f gpurun_out/${tag}_source.csv
+done
+timeout 1500 python tools/parity_report.py > gpurun_out/parity.json 2> gpurun_out/parity.err; echo "parity rc=$?"

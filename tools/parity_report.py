@@ -1,45 +1,65 @@
-"""Parity + timing report of the BASELINE configs on the GPU.
+"""Parity + timing report on the GPU against the REAL reference's full-size runs.
 
-    python tools/parity_report.py [cfg1 cfg2 ...] > gpurun_out/parity.json
+    python tools/parity_report.py [case ...] > gpurun_out/parity.json
 
-For every config with a full-size residual history of the REAL reference in
-tests/golden/histories.json (made by tests/golden/make_golden.py --full):
-iteration count, converged flag, max_k |r_k - r_k^ref| / r_0^ref, and the
-per-iteration relative deviation for the iterations with r_k / r_0 >= 1e-4
-(SURVEY 8c's contract).  cfg5 (2^14 x 2^20, 137 GB iterate) runs at a reduced
-n_t (the n_x = 16384 row length is exercised in full) and reports convergence
-only: there is no reference history at that size.
+Cases are the fixtures of tests/golden/full (made by tests/golden/make_full.py
+with the real reference: residual history, iteration count, final-iterate
+samples; `<case>_reordered` = the oracle with reordered GMRES reductions, the
+reference's own reduction-order envelope): cfg1-cfg4 at full size and the
+cfg4 / cfg5 proxies.  Per case: iterations, max_k |r_k - r_k^ref| / r_0, the
+relative deviation while r_k >= 1e-4 r_0, the final-iterate deviation (17
+sampled rows, relative l2; every row's l2 norm, max relative) next to the same
+figures of the envelope run, and the time to tolerance.
 """
 import json
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2209_06916_b200 as P  # noqa: E402
 from paper_2209_06916_b200.configs import CONFIGS  # noqa: E402
 
-hist = json.load(open(os.path.join(ROOT, "tests", "golden", "histories.json")))
-names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5@16384x16384"]
+FULL = os.path.join(ROOT, "tests", "golden", "full")
+CASES = {"cfg1": ("cfg1", None, None), "cfg2": ("cfg2", None, None), "cfg3": ("cfg3", None, None),
+         "cfg4": ("cfg4", None, None), "cfg4p": ("cfg4", 1024, 65536),
+         "cfg5p": ("cfg5", 16384, 16384), "cfg5q": ("cfg5", 16384, 131072)}
+
+
+def load(name):
+    path = os.path.join(FULL, name + ".json")
+    if not os.path.exists(path):
+        return None, None
+    return json.load(open(path)), np.load(os.path.join(FULL, name + "_final.npz"))
+
+
+def final_dev(fa, fb):
+    ds = np.linalg.norm(fa["samples"] - fb["samples"]) / np.linalg.norm(fb["samples"])
+    dn = np.max(np.abs(fa["row_norms"] - fb["row_norms"]) / np.maximum(fb["row_norms"], 1e-300))
+    return float(ds), float(dn)
+
+
 out = {}
-for name in names:
-    if "@" in name:
-        base, size = name.split("@")
-        nx, nt = (int(v) for v in size.split("x"))
-        cf = CONFIGS[base].scaled(nx, nt)
-    else:
-        cf = CONFIGS[name]
+for name in sys.argv[1:] or list(CASES):
+    ref, fref = load(name)
+    if ref is None:
+        continue
+    base, n_x, n_t = CASES[name]
+    cf = CONFIGS[base]
+    if cf.cycle == "f_cycle":
+        cf = cf.as_v_cycle()  # the reference has no F-cycle
+    if n_x:
+        cf = cf.scaled(n_x, n_t)
     prob = cf.problem()
-    cfg = P.MgritConfig(nu=1, cycle=cf.cycle, tol=1e-10, max_iters=30, rng_seed=0)
-    solver = P.MgritSolver(prob, cfg)
-    u_host = solver.initial_state()
-    ud = torch.from_numpy(u_host).cuda()
+    solver = P.MgritSolver(prob, P.MgritConfig(cycle=cf.cycle))
+    ud = torch.from_numpy(solver.initial_state()).cuda()
     solver.solve(ud.clone())  # warm-up (plans, workspaces)
     u = ud.clone()
+    del ud
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
@@ -47,20 +67,32 @@ for name in names:
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
-    row = {"n_x": cf.n_x, "n_t": cf.n_t, "iterations": rep.iterations, "converged": rep.converged,
+    un = u.cpu().numpy()
+    del u
+    mine = {"samples": un[fref["rows"]], "row_norms": np.sqrt(np.einsum("ij,ij->i", un, un))}
+    del un
+    r0 = ref["norms"][0]
+    rel = [abs(a - b) / b for a, b in zip(rep.residual_norms, ref["norms"]) if b / r0 >= 1e-4]
+    ds, dn = final_dev(mine, fref)
+    row = {"n_x": cf.n_x, "n_t": cf.n_t, "cycle": cf.cycle, "iterations": rep.iterations,
+           "reference_iterations": ref["iterations"], "converged": rep.converged,
            "final_ratio": rep.residual_norms[-1] / rep.residual_norms[0],
-           "time_to_tolerance_ms": ms, "dof_per_s": cf.n_x * cf.n_t / (ms / 1e3)}
-    ref = hist.get(name)
-    if ref is not None:
-        r0 = ref["norms"][0]
-        row["reference_iterations"] = ref["iterations"]
-        row["reference_wall_s"] = ref.get("wall")
-        row["max_abs_dev_over_r0"] = max(abs(a - b) / r0 for a, b in zip(rep.residual_norms, ref["norms"]))
-        rel = [abs(a - b) / b for a, b in zip(rep.residual_norms, ref["norms"]) if b / r0 >= 1e-4]
-        row["max_rel_dev_while_r_ge_1e-4_r0"] = max(rel) if rel else None
-        row["same_iterations"] = rep.iterations == ref["iterations"]
+           "history_max_abs_dev_over_r0": max(abs(a - b) / r0
+                                              for a, b in zip(rep.residual_norms, ref["norms"])),
+           "history_max_rel_dev_while_r_ge_1e-4_r0": max(rel) if rel else None,
+           "final_iterate_sampled_rows_rel_l2": ds, "final_iterate_row_norms_max_rel": dn,
+           "time_to_tolerance_ms": ms, "dof_per_s": cf.n_x * cf.n_t / (ms / 1e3),
+           "reference_wall_s": ref.get("wall")}
+    env, fenv = load(name + "_reordered")
+    if env is not None:
+        es, en = final_dev(fenv, fref)
+        row["envelope"] = {"iterations": env["iterations"],
+                           "history_max_abs_dev_over_r0": max(abs(a - b) / r0 for a, b in
+                                                              zip(env["norms"], ref["norms"])),
+                           "final_iterate_sampled_rows_rel_l2": es,
+                           "final_iterate_row_norms_max_rel": en}
     out[name] = row
     print(json.dumps({name: row}), file=sys.stderr, flush=True)
-    del u, ud, solver
+    del solver
     torch.cuda.empty_cache()
 print(json.dumps(out, indent=1))
