@@ -7,3 +7,5 @@ ncu --set full --clock-control none --import-source on --profile-from-start off 
 ncu -i gpurun_out/${tag}.ncu-rep --page details --csv > gpurun_out/${tag}_details.csv 2>/dev/null
 ncu -i gpurun_out/${tag}.ncu-rep --page raw --csv > gpurun_out/${tag}_raw.csv 2>/dev/null
 ncu -i gpurun_out/${tag}.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${tag}_source.csv 2>/dev/null
+# keep the call's output under gpurun's 64 MiB merge limit: the CSV pages above are what is read
+rm -f gpurun_out/${tag}.ncu-rep gpurun_out/${tag}_details.csv
