@@ -25,6 +25,9 @@ CASES = {  # family, p, c, n_x, n_t, m, cycle, nu
     "erk3_f_cycle": ("erk", 3, 0.85, 64, 256, 4, "f_cycle", 1),
     "erk1_v_nu0": ("erk", 1, 0.85, 32, 256, 2, "v_cycle", 0),
     "erk3_v_nu2": ("erk", 3, 0.85, 32, 256, 4, "v_cycle", 2),
+    # BASELINE cfg5's scheme (ERK3 + U3, c = 0.85, m = 8, F-cycle over five levels, GMRES-
+    # corrected coarse operators) at a reduced grid
+    "cfg5_reduced_f_cycle": ("erk", 3, 0.85, 32, 4096, 8, "f_cycle", 1),
 }
 
 
