@@ -152,20 +152,10 @@ __device__ __forceinline__ void c1_mbar_wait(uint64_t* bar, uint32_t parity) {
 // (I - phi D) on warp scratch: out at x from src[x - R .. x + R], exact mode
 template <int R>
 __device__ __forceinline__ double c1_A(const double (&w)[2 * R + 1], const double* src, int x) {
-#ifdef MGB_C1_ILP
-  // two partial sums (taps 0..R and R+1..2R): half the dependent-add chain
-  double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-  for (int d = 0; d <= R; ++d) s0 = __dadd_rn(s0, __dmul_rn(w[d], src[x - R + d]));
-#pragma unroll
-  for (int d = R + 1; d <= 2 * R; ++d) s1 = __dadd_rn(s1, __dmul_rn(w[d], src[x - R + d]));
-  return __dadd_rn(s0, s1);
-#else
   double s = 0.0;
 #pragma unroll
   for (int d = 0; d <= 2 * R; ++d) s = __dadd_rn(s, __dmul_rn(w[d], src[x - R + d]));
   return s;
-#endif
 }
 
 // halo'd basis row i: shared memory for i < K, else the CTA's workspace slot
@@ -243,22 +233,6 @@ __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
     const double* vr = lane <= j ? c1_row<OVF>(c, lane) + c.seg : (lane == j + 1 ? uu : c.zx + off);
     const double2* v2 = reinterpret_cast<const double2*>(vr);
     const double2* u2 = reinterpret_cast<const double2*>(uu);
-#ifdef MGB_C1_ILP
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
-    for (int e = 0; e < S / 2; e += 4) {  // S = 32 SEGK: S / 2 is a multiple of 4 for SEGK >= 1... (16, 32)
-      const double2 x0 = v2[e], x1 = v2[e + 1], x2 = v2[e + 2], x3 = v2[e + 3];
-      const double2 y0 = u2[e], y1 = u2[e + 1], y2 = u2[e + 2], y3 = u2[e + 3];
-      a0 = fma(x0.x, y0.x, a0);
-      a1 = fma(x0.y, y0.y, a1);
-      a2 = fma(x1.x, y1.x, a2);
-      a3 = fma(x1.y, y1.y, a3);
-      b0 = fma(x2.x, y2.x, b0);
-      b1 = fma(x2.y, y2.y, b1);
-      b2 = fma(x3.x, y3.x, b2);
-      b3 = fma(x3.y, y3.y, b3);
-    }
-    c.wred[c.warp * C1_SLOTS + lane] = ((a0 + a1) + (a2 + a3)) + ((b0 + b1) + (b2 + b3));
-#else
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int e = 0; e < S / 2; e += 2) {
       const double2 x0 = v2[e], x1 = v2[e + 1], y0 = u2[e], y1 = u2[e + 1];
@@ -268,7 +242,6 @@ __device__ __forceinline__ void c1_dots(C1Ctx& c, int j) {
       a3 = fma(x1.y, y1.y, a3);
     }
     c.wred[c.warp * C1_SLOTS + lane] = (a0 + a1) + (a2 + a3);
-#endif
   }
 }
 
@@ -431,11 +404,6 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
           const int xx = lane + 32 * k;
           v[k] = xx < XE ? Uh[e0 + xx] : 0.0;
         }
-#ifdef MGB_C1_ILP
-        double vo[KX];  // odd rows accumulate separately: half the dependent FMA chain
-#pragma unroll
-        for (int k = 0; k < KX; ++k) vo[k] = 0.0;
-#endif
 #pragma unroll
         for (int i0 = 0; i0 < CAP; i0 += 4) {
           if (i0 < j) {
@@ -448,19 +416,11 @@ __device__ void c1_step(C1Ctx& c, cg::cluster_group& cl, double (&x)[SEGK], int&
               for (int k = 0; k < KX; ++k) {
                 const int xx = lane + 32 * k;
                 const double vi = (i < j && xx < XE) ? Vi[xx] : 0.0;
-#ifdef MGB_C1_ILP
-                if (ii & 1) vo[k] = fma(-a_b, vi, vo[k]); else v[k] = fma(-a_b, vi, v[k]);
-#else
                 v[k] = fma(-a_b, vi, v[k]);
-#endif
               }
             }
           }
         }
-#ifdef MGB_C1_ILP
-#pragma unroll
-        for (int k = 0; k < KX; ++k) v[k] += vo[k];
-#endif
       }
       CL_TR(13)
       asm volatile("bar.sync 2, %0;" ::"r"(nthr) : "memory");
