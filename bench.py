@@ -52,6 +52,17 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK_GBS = 6650.0
 
 
+def resolve_config(name: str):
+    """``cfgN`` or a reduced grid of one, ``cfgN@<n_x>x<n_t>`` (tooling: per-pass
+    timings of cfg5's 16384-point rows on one GPU)."""
+    from paper_2209_06916_b200.configs import CONFIGS
+    if "@" in name:
+        base, size = name.split("@")
+        n_x, n_t = (int(v) for v in size.split("x"))
+        return CONFIGS[base].scaled(n_x, n_t)
+    return CONFIGS[name]
+
+
 def workload(cf) -> str:
     """The workload named in every bench line (both arms, every N)."""
     return (f"{cf.name}: {cf.family.upper()}{cf.p}+U{cf.p} c={cf.c} n_x={cf.n_x} n_t={cf.n_t} "
@@ -279,7 +290,7 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cf = CONFIGS[args.config]
+    cf = resolve_config(args.config)
     prob = cf.problem()
     cfg = P.MgritConfig(nu=1, cycle=cf.cycle, tol=1e-10, max_iters=30, rng_seed=0)
     if world > 1:
@@ -577,7 +588,7 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2209_06916_b200.configs import CONFIGS
-    cf = CONFIGS[args.config]
+    cf = resolve_config(args.config)
     thr = os.cpu_count() or 1
     for _ in range(args.warmup):
         oracle_sample(cf, threads=thr)

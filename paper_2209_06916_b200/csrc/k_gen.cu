@@ -8,7 +8,19 @@ namespace mgb {
   MGB_REG(K_GEN, P, 0, 1, false); \
   MGB_REG(K_SLD, P, 0, 1, true);  \
   MGB_REG(K_SLG, P, 0, 1, true);
+// dedicated SL + direct-solve kernel: key span = 200 + SL stencil span (= order p; 0 when the
+// departure points fall on the mesh: integer coarse CFL numbers, cfg3)
+#define SLD_P(P)                                                                                     \
+  register_kernel(KernelKey{K_SLD, P, 200, 1, 1}, reinterpret_cast<const void*>(&relax_sld_kernel<P, 0>)); \
+  register_kernel(KernelKey{K_SLD, P, 201, 1, 1}, reinterpret_cast<const void*>(&relax_sld_kernel<P, 1>)); \
+  register_kernel(KernelKey{K_SLD, P, 202, 1, 1}, reinterpret_cast<const void*>(&relax_sld_kernel<P, 2>)); \
+  register_kernel(KernelKey{K_SLD, P, 203, 1, 1}, reinterpret_cast<const void*>(&relax_sld_kernel<P, 3>)); \
+  register_kernel(KernelKey{K_SLD, P, 204, 1, 1}, reinterpret_cast<const void*>(&relax_sld_kernel<P, 4>)); \
+  register_kernel(KernelKey{K_SLD, P, 205, 1, 1}, reinterpret_cast<const void*>(&relax_sld_kernel<P, 5>));
 void register_gen() {
+  SLD_P(4)
+  SLD_P(8)
+  SLD_P(16)
   // register-rich GMRES variants for T <= 256 (key: nst = 2)
   register_kernel(KernelKey{K_SLG, 16, 0, 2, 1},
                   reinterpret_cast<const void*>(&relax_kernel<16, K_SLG, 0, 1, true, 256>));

@@ -99,9 +99,23 @@ static_assert(sizeof(StepParams) % 16 == 0, "StepParams must be 16-byte sized");
 constexpr int RKD_MAXF = 3;   // factors of the stage operator
 constexpr int RKD_MAXP = 8;   // points per thread
 constexpr int RKD_KMAX = 16;  // longest carry window (chunks)
+constexpr int WIN_X = 4;      // wrap replica columns of a resident slice (fixed-geometry / SLD kernels)
 struct RkdFactor {
   double a1, a2, M[4], h1[RKD_MAXP], h2[RKD_MAXP];
   int dir, win;
+};
+// factor of the dedicated SL + direct-solve kernel: up to 16 points per thread and
+// the tables of the hierarchical scan (slow-decaying factors: win == 0)
+struct SldFactor {
+  double a1, a2, M[4], h1[16], h2[16];
+  double Mpow[10][4];  // M^(2^k): lane scan (k < 5), warp scan (k >= 5)
+  double Winv[4];      // (I - M^T)^-1: periodic closure
+  int dir, win;
+};
+struct SldConst {
+  SldFactor f[2];
+  double gain_inv;
+  int nfac, pad_;
 };
 struct RkdConst {
   RkdFactor f[RKD_MAXF];
@@ -117,6 +131,7 @@ struct RelaxLaunch {
   // the constant bank, so every tap weight is an instruction operand, not a register
   double win_w[32];
   RkdConst rk;
+  SldConst sd;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -264,8 +279,10 @@ __device__ __forceinline__ void stencil_gen(const Ctx& c, int ntap, const int* o
   }
 }
 
-// contiguous short stencil: each thread loads a register window of P+SPAN
-// neighbours once and produces P outputs (reuse factor (SPAN+1)P/(P+SPAN)).
+// contiguous short stencil through a register window: outputs in part-chunks of
+// H points from a window of H + SPAN neighbours (reuse factor (SPAN+1)H/(H+SPAN)).
+// The whole chunk at once (H = P) for up to 16 points per thread; 8-point parts
+// for 32 points per thread (n_x = 16384), whose full window spilled registers.
 template <int P, int SPAN, bool EXACT>
 __device__ __forceinline__ void stencil_win(const Ctx& c, int tb, int r0, const double (&wd)[SPAN + 1],
                                             double (&y)[P]) {
@@ -274,20 +291,25 @@ __device__ __forceinline__ void stencil_win(const Ctx& c, int tb, int r0, const 
     for (int q = 0; q < P; ++q) y[q] = 0.0;
     return;
   }
-  double win[P + SPAN];
+  constexpr int H = P > 16 ? 8 : P;
 #pragma unroll
-  for (int w = 0; w < P + SPAN; ++w) {
-    const int cw = r0 + w;
-    int tt = tb + cw / P;
-    tt = tt >= c.T ? tt - c.T : tt;
-    win[w] = c.row[(cw & (P - 1)) * c.S + tt];
-  }
+  for (int h = 0; h < P; h += H) {
+    double win[H + SPAN];
 #pragma unroll
-  for (int q = 0; q < P; ++q) {
-    double acc = 0.0;
+    for (int w = 0; w < H + SPAN; ++w) {
+      const int cw = r0 + h + w;
+      int tt = tb + cw / P;
+      tt = tt >= c.T ? tt - c.T : tt;
+      tt = tt >= c.T ? tt - c.T : tt;
+      win[w] = c.row[(cw & (P - 1)) * c.S + tt];
+    }
 #pragma unroll
-    for (int k = 0; k <= SPAN; ++k) acc = madd<EXACT>(acc, wd[k], win[q + k]);
-    y[q] = acc;
+    for (int q = 0; q < H; ++q) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k <= SPAN; ++k) acc = madd<EXACT>(acc, wd[k], win[q + k]);
+      y[h + q] = acc;
+    }
   }
 }
 
@@ -1598,6 +1620,314 @@ __global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const Step
   }
 }
 
+// ------------------------------------------- SL + direct correction solve
+// Dedicated kernel for the corrected semi-Lagrangian coarse steps with a direct
+// solve (stepping.py:546-551: x = (I - phi D)^-1 SL u): the SL interpolation
+// stencil is a contiguous window at a far offset (read from the resident row
+// through a register window: double-buffered slice with wrap replicas, one CTA
+// barrier per step besides the factors'), the factor solves take their
+// coefficients and scan tables from the kernel parameters (constant bank) and
+// rows move between registers and HBM directly.  Fast-decaying factors use the
+// windowed carries of rkd_factor, slow-decaying ones (deep levels) the
+// hierarchical scan of chain_solve (warp Kogge-Stone, warp 0 over the warp
+// totals with the periodic closure); same operations in the same order as the
+// generic kernel.
+template <int P, bool FWD>
+__device__ __forceinline__ void sld_factor(const SldFactor& F, double2* wb, double* st, int t, int T,
+                                           double (&x)[P]) {
+  const int tl = FWD ? t : T - 1 - t;
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int qq = 0; qq < P; ++qq) {
+    const int q = FWD ? qq : P - 1 - qq;
+    const double yv = fma(F.a1, s1, fma(F.a2, s2, x[q]));
+    x[q] = yv;
+    s2 = s1;
+    s1 = yv;
+  }
+  double c1 = 0.0, c2 = 0.0;
+  if (F.win > 0) {
+    wb[tl + RKD_KMAX] = make_double2(s1, s2);
+    if (tl >= T - RKD_KMAX) wb[tl + RKD_KMAX - T] = make_double2(s1, s2);
+    __syncthreads();
+    const int K = F.win;
+    const double2* p = wb + tl + RKD_KMAX - K;  // chunks tl - K .. tl - 1
+#pragma unroll 2
+    for (int k = 0; k < K; ++k) {
+      const double2 bb = p[k];
+      const double n1 = fma(F.M[0], c1, F.M[1] * c2);
+      const double n2 = fma(F.M[2], c1, F.M[3] * c2);
+      c1 = n1 + bb.x;
+      c2 = n2 + bb.y;
+    }
+  } else {
+    // hierarchical scan over logical chunks (T a multiple of 32)
+    double* cin = st + 64;
+    const int NW = T >> 5, lane = t & 31, w = t >> 5;
+    const int ll = FWD ? lane : 31 - lane;
+    const int lw = FWD ? w : NW - 1 - w;
+    double y1 = s1, y2 = s2;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+      const int off = 1 << d;
+      const int src = (FWD ? lane - off : lane + off) & 31;
+      double p1 = __shfl_sync(0xffffffffu, y1, src), p2 = __shfl_sync(0xffffffffu, y2, src);
+      if (ll >= off) {
+        const double n1 = fma(F.Mpow[d][0], p1, F.Mpow[d][1] * p2);
+        const double n2 = fma(F.Mpow[d][2], p1, F.Mpow[d][3] * p2);
+        y1 += n1;
+        y2 += n2;
+      }
+    }
+    const int s1src = (FWD ? lane - 1 : lane + 1) & 31;
+    double e1 = __shfl_sync(0xffffffffu, y1, s1src), e2 = __shfl_sync(0xffffffffu, y2, s1src);
+    if (ll == 0) e1 = e2 = 0.0;
+    if (ll == 31) {
+      st[lw] = y1;
+      st[32 + lw] = y2;
+    }
+    __syncthreads();
+    if (w == 0) {
+      double a1w = lane < NW ? st[lane] : 0.0, a2w = lane < NW ? st[32 + lane] : 0.0;
+#pragma unroll
+      for (int d = 0; d < 5; ++d) {
+        const int off = 1 << d;
+        double p1 = __shfl_up_sync(0xffffffffu, a1w, off), p2 = __shfl_up_sync(0xffffffffu, a2w, off);
+        if (lane >= off) {
+          const double n1 = fma(F.Mpow[5 + d][0], p1, F.Mpow[5 + d][1] * p2);
+          const double n2 = fma(F.Mpow[5 + d][2], p1, F.Mpow[5 + d][3] * p2);
+          a1w += n1;
+          a2w += n2;
+        }
+      }
+      double z1 = __shfl_sync(0xffffffffu, a1w, NW - 1), z2 = __shfl_sync(0xffffffffu, a2w, NW - 1);
+      {  // s_{-1}: periodic closure
+        const double n1 = fma(F.Winv[0], z1, F.Winv[1] * z2);
+        const double n2 = fma(F.Winv[2], z1, F.Winv[3] * z2);
+        z1 = n1;
+        z2 = n2;
+      }
+      double x1 = __shfl_up_sync(0xffffffffu, a1w, 1), x2 = __shfl_up_sync(0xffffffffu, a2w, 1);
+      if (lane == 0) x1 = x2 = 0.0;
+#pragma unroll
+      for (int d = 0; d < 5; ++d)
+        if ((lane >> d) & 1) {  // (M^32)^lw s_{-1}
+          const double n1 = fma(F.Mpow[5 + d][0], z1, F.Mpow[5 + d][1] * z2);
+          const double n2 = fma(F.Mpow[5 + d][2], z1, F.Mpow[5 + d][3] * z2);
+          z1 = n1;
+          z2 = n2;
+        }
+      if (lane < NW) {
+        cin[lane] = x1 + z1;
+        cin[32 + lane] = x2 + z2;
+      }
+    }
+    __syncthreads();
+    c1 = cin[lw];
+    c2 = cin[32 + lw];
+#pragma unroll
+    for (int d = 0; d < 5; ++d)
+      if ((ll >> d) & 1) {  // M^ll C_w
+        const double n1 = fma(F.Mpow[d][0], c1, F.Mpow[d][1] * c2);
+        const double n2 = fma(F.Mpow[d][2], c1, F.Mpow[d][3] * c2);
+        c1 = n1;
+        c2 = n2;
+      }
+    c1 += e1;
+    c2 += e2;
+  }
+#pragma unroll
+  for (int qq = 0; qq < P; ++qq) {
+    const int q = FWD ? qq : P - 1 - qq;
+    x[q] = fma(F.h1[qq], c1, fma(F.h2[qq], c2, x[q]));
+  }
+}
+
+template <int P, int SPAN>
+__global__ void __launch_bounds__(512, 1) relax_sld_kernel(const StepParams* __restrict__ gp,
+                                                           const RelaxLaunch L) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const mgb_relax_args& a = L.a;
+  const SldConst& sd = L.sd;
+  const int n = gp->n, T = gp->T, t = threadIdx.x;  // T == blockDim.x, a multiple of 32
+  const int S = T + WIN_X;                           // chunk row + wrap replica columns
+  const int lo = gp->win_lo, reps = gp->repeat;
+  int tb = t + lo / P;
+  tb = tb >= T ? tb - T : tb;
+  const int r0 = lo & (P - 1);
+  // shared layout (doubles): red[64] | st/cin[128] | wb[2][T + RKD_KMAX] pairs | row[2][P][S]
+  double* base = reinterpret_cast<double*>(smem_raw);
+  Ctx c;
+  c.red = base;
+  c.parity = 0;
+  c.T = T;
+  c.t = t;
+  double* st = base + 64;
+  double2* wb = reinterpret_cast<double2*>(base + 192);
+  double* row0 = base + 192 + 4 * (T + RKD_KMAX);
+  const int PS = P * S;
+  double wd[SPAN + 1];
+#pragma unroll
+  for (int k = 0; k <= SPAN; ++k) wd[k] = L.win_w[k];
+
+  for (long long k = blockIdx.x; k < a.n_intervals; k += gridDim.x) {
+    const long long kg = a.k_global0 + k;
+    const long long rowbase = k * (long long)a.m;
+    double y[P];
+    const double* csrc = (kg == 0 && a.c_src0) ? a.c_src0 : (a.c_src ? a.c_src + k * a.c_stride : nullptr);
+    if (csrc) {
+      load_chunk<P>(csrc, t, y);
+    } else {
+#pragma unroll
+      for (int q = 0; q < P; ++q) y[q] = 0.0;
+    }
+    if (a.e && kg >= 1) {  // u[m::m] += e[1:] (mgrit.py:246)
+      double ev[P];
+      load_chunk<P>(a.e + k * a.e_stride, t, ev);
+#pragma unroll
+      for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], ev[q]);
+    }
+    if (a.c_out) store_chunk<P>(a.c_out + k * a.c_out_stride, t, y);
+    int cur = 0;
+    __syncthreads();  // previous interval's readers of both row buffers are done
+    {
+      double* row = row0;
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        row[q * S + t] = y[q];
+        if (t < WIN_X) row[q * S + T + t] = y[q];
+      }
+    }
+    __syncthreads();
+    const int nsteps = a.n_fsteps + (a.tail ? 1 : 0);
+    for (int j = 1; j <= nsteps; ++j) {
+      const bool is_tail = j > a.n_fsteps;
+      const long long grow = is_tail ? rowbase + a.m : rowbase + j;
+      if (a.g) {  // this step's rhs chunk into L1 while the step runs
+        const double* gp1 = a.g + grow * n + (size_t)t * P;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(gp1));
+      }
+      for (int r = 0; r < reps; ++r) {
+        // ---- b = SL(row): register window at the departure offset, exact rolled sum
+        const double* src = row0 + cur * PS;
+        {
+          double win[P + SPAN];
+#pragma unroll
+          for (int w = 0; w < P + SPAN; ++w) {
+            const int cw = r0 + w;
+            win[w] = src[(cw & (P - 1)) * S + tb + cw / P];
+          }
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            double acc = 0.0;
+#pragma unroll
+            for (int kk = 0; kk <= SPAN; ++kk) acc = madd<true>(acc, wd[kk], win[q + kk]);
+            y[q] = acc;
+          }
+        }
+        // ---- x = (I - phi D)^-1 b: factorised periodic solve
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          if (f < sd.nfac) {
+            double2* wbf = wb + f * (T + RKD_KMAX);
+            if (sd.f[f].dir > 0)
+              sld_factor<P, true>(sd.f[f], wbf, st, t, T, y);
+            else
+              sld_factor<P, false>(sd.f[f], wbf, st, t, T, y);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) y[q] *= sd.gain_inv;
+        if (r + 1 < reps) {
+          double* dst = row0 + (cur ^ 1) * PS;
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            dst[q * S + t] = y[q];
+            if (t < WIN_X) dst[q * S + T + t] = y[q];
+          }
+          cur ^= 1;
+          __syncthreads();
+        }
+      }
+      if (!is_tail) {
+        if (a.g) {
+          double gv[P];
+          load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+          for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], gv[q]);  // upd + g (mgrit.py:142)
+        }
+        if (a.write_f == 2 || (a.write_f == 1 && j == a.n_fsteps)) store_chunk<P>(a.u + grow * n, t, y);
+        if (j < nsteps) {  // republish for the next step
+          double* dst = row0 + (cur ^ 1) * PS;
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            dst[q * S + t] = y[q];
+            if (t < WIN_X) dst[q * S + T + t] = y[q];
+          }
+          cur ^= 1;
+          __syncthreads();
+        }
+      } else if (a.tail == 1) {  // C-relaxation (mgrit.py:148-149)
+        if (a.g) {
+          double gv[P];
+          load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+          for (int q = 0; q < P; ++q) y[q] = __dadd_rn(y[q], gv[q]);
+        }
+        store_chunk<P>(a.tail_out + k * a.tail_stride, t, y);
+      } else {  // residual g + Phi u - u_C (mgrit.py:159-161)
+        double part = 0.0;
+        double rr[P];
+        if (a.g) {
+          double gv[P];
+          load_chunk<P>(a.g + grow * n, t, gv);
+#pragma unroll
+          for (int q = 0; q < P; ++q) rr[q] = __dadd_rn(gv[q], y[q]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < P; ++q) rr[q] = y[q];
+        }
+        {
+          double cr[P];
+          load_chunk<P>(a.cref + k * a.cref_stride, t, cr);
+          if (a.cref_e) {
+            double ev[P];
+            load_chunk<P>(a.cref_e + k * a.cref_e_stride, t, ev);
+#pragma unroll
+            for (int q = 0; q < P; ++q) cr[q] = __dadd_rn(cr[q], ev[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            rr[q] = __dsub_rn(rr[q], cr[q]);
+            part = fma(rr[q], rr[q], part);
+          }
+        }
+        if (a.tail_out) store_chunk<P>(a.tail_out + k * a.tail_stride, t, rr);
+        if (a.partials) {
+          const double sum = block_sum(c, part);
+          if (t == 0) a.partials[k] = sum;
+        }
+      }
+    }
+    if (a.c_last_out && k == a.n_intervals - 1) {  // final C-point (k+1 >= 1)
+      double cl[P];
+      if (a.c_src) {
+        load_chunk<P>(a.c_src + (k + 1) * a.c_stride, t, cl);
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) cl[q] = 0.0;
+      }
+      if (a.e) {
+        double ev[P];
+        load_chunk<P>(a.e + (k + 1) * a.e_stride, t, ev);
+#pragma unroll
+        for (int q = 0; q < P; ++q) cl[q] = __dadd_rn(cl[q], ev[q]);
+      }
+      store_chunk<P>(a.c_last_out, t, cl);
+    }
+  }
+}
+
 // ------------------------------------------- explicit-stencil relaxation
 // Dedicated kernel for assembled explicit stencils (the fine ERK levels):
 // stencil weights are kernel parameters (constant-bank operands, no registers),
@@ -1619,7 +1949,6 @@ __device__ __forceinline__ void slice_store2(const double* row, double* dst, int
 // stride is the constant WIN_S<TT> and every chunk row is extended by WIN_X
 // columns that replicate columns 0..WIN_X-1 (the periodic wrap), so a window
 // read is base + immediate: no wrap arithmetic and no address registers.
-constexpr int WIN_X = 4;
 template <int TT>
 struct WinGeo {
   static constexpr int S = TT + 17;  // == 1 (mod 16): conflict-free rows and natural-order copies

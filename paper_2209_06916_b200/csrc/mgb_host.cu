@@ -48,6 +48,7 @@ struct Tuning {
   bool slg_no_occ2 = false;   // MGB_SLG_NO_OCC2: no 2-CTA/SM single-CTA GMRES build
   bool rk_stencil = false;    // MGB_RK_STENCIL: SDIRK stage values by the stencil in fast mode too
   bool no_rkd = false;        // MGB_NO_RKD: staged SDIRK on the generic kernel
+  bool no_sld = false;        // MGB_NO_SLD: SL + direct solve on the generic kernel
   long long max_grid = 0;     // MGB_MAX_GRID: cap the grid (tests: many intervals per CTA)
 };
 const Tuning& tuning() {
@@ -68,6 +69,7 @@ const Tuning& tuning() {
     x.slg_no_occ2 = flag("MGB_SLG_NO_OCC2");
     x.rk_stencil = flag("MGB_RK_STENCIL");
     x.no_rkd = flag("MGB_NO_RKD");
+    x.no_sld = flag("MGB_NO_SLD");
     x.max_grid = num("MGB_MAX_GRID", 0);
     return x;
   }();
@@ -408,6 +410,7 @@ struct mgb_step {
   int dkind = 0, P = 1, T = 1, S = 1, span = 0, nst = 1, exact = 1;
   bool vec16 = false;  // relax_win_kernel: 16-byte row accesses
   mgb::RkdConst rk = {};  // relax_rkd_kernel constants
+  mgb::SldConst sd = {};  // relax_sld_kernel constants
   int threads = 32, smem = 0, max_grid = 1, sms = 148;
   const void* fn = nullptr;
   // SL_GMRES single-CTA: 2 CTAs/SM variant for levels that need > 1 wave of fn
@@ -802,6 +805,40 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
     if (allwin && ((HL == 1 && HR == 0) || (HL == 2 && HR == 1) || (HL == 3 && HR == 2)))
       rkd_key = 100 + 10 * HL + HR;
   }
+  // dedicated SL + direct-solve kernel: contiguous SL stencil of span 0..5, at most two
+  // factors (first / second order), no symbol shift, whole warps
+  int sld_key = 0;
+  if (dk == mgb::K_SLD && !tuning().no_sld && P >= 4 && P <= 16 && T % 32 == 0 && T <= 512 &&
+      hp.shift == 0 && hp.nfac >= 1 && hp.nfac <= 2 && d->n_taps >= 1 && d->n_taps <= 6) {
+    bool contig = true;
+    for (int k = 1; k < d->n_taps; ++k) contig = contig && off[k] == off[0] + k;
+    if (contig) {
+      sld_key = 200 + d->n_taps - 1;
+      hp.win_lo = (int)mod_n(off[0], n);
+      hp.win_span = d->n_taps - 1;
+      for (int k = 0; k < d->n_taps; ++k) hp.win_w[k] = d->weights[k];
+      st->smem = (int)(8 * (192 + 4 * (size_t)(T + mgb::RKD_KMAX) + 2 * (size_t)P * (T + mgb::WIN_X)));
+      mgb::SldConst& sd = st->sd;
+      std::memset(&sd, 0, sizeof(sd));
+      sd.nfac = hp.nfac;
+      sd.gain_inv = hp.gain_inv;
+      for (int f = 0; f < hp.nfac; ++f) {
+        const Factor& F = hp.fac[f];
+        mgb::SldFactor& R = sd.f[f];
+        R.a1 = F.a1; R.a2 = F.a2; R.dir = F.dir; R.win = F.win;
+        for (int k = 0; k < 4; ++k) { R.M[k] = F.M[k]; R.Winv[k] = F.Winv[k]; }
+        for (int q = 0; q < P; ++q) { R.h1[q] = F.h1[q]; R.h2[q] = F.h2[q]; }
+        for (int e = 0; e < 10; ++e)
+          for (int k = 0; k < 4; ++k) R.Mpow[e][k] = F.Mpow[e][k];
+      }
+    }
+  }
+  if (tuning().debug && dk == mgb::K_SLD) {
+    fprintf(stderr, "[mgb] sld n=%d P=%d T=%d shift=%d nfac=%d ntaps=%d key=%d offsets:", n, P, T, hp.shift, hp.nfac,
+            (int)d->n_taps, sld_key);
+    for (int k = 0; k < d->n_taps; ++k) fprintf(stderr, " %lld", off[k]);
+    fprintf(stderr, "\n");
+  }
   if (rkd_key) {
     st->smem = (int)(sizeof(StepParams) + 8 * (72 + 4 * (size_t)(T + mgb::RKD_KMAX) + (size_t)hp.win_span * T +
                                                (size_t)(hp.stages - 1) * P * T));
@@ -849,6 +886,7 @@ int mgb_step_create(const mgb_step_desc* d, mgb_step** out) {
       it = registry().find(std::make_tuple(dk, P, span, 2, st->exact));
     if (win_fixed) it = registry().find(std::make_tuple(dk, P, span, T == 512 ? 3 : 4, st->exact));
     if (rkd_key) it = registry().find(std::make_tuple(dk, P, rkd_key, st->nst, st->exact));
+    if (sld_key) it = registry().find(std::make_tuple(dk, P, sld_key, 1, 1));
     if (it == registry().end()) it = registry().find(std::make_tuple(dk, P, span, st->nst, st->exact));
     if (it == registry().end()) { delete st; return fail(MGB_ERR_UNSUPPORTED, "no kernel instantiation for this layout"); }
     st->fn = it->second;
@@ -943,6 +981,7 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   L.ws_slot = 0;
   std::memcpy(L.win_w, st->hp.win_w, sizeof(L.win_w));
   L.rk = st->rk;
+  L.sd = st->sd;
   long long grid = std::min<long long>(a->n_intervals, st->max_grid);
   // tooling / tests only: cap the grid so that every CTA walks a block of
   // several intervals (the chained head/tail hand-off of relax_win_kernel)

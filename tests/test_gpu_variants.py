@@ -1,6 +1,7 @@
 """Kernel variants that must agree bit for bit: the dedicated SDIRK kernel
-(relax_rkd_kernel) against the generic staged kernel it replaces (MGB_NO_RKD=1,
-read once per process: the generic run is a subprocess)."""
+(relax_rkd_kernel) and the dedicated SL + direct-solve kernel (relax_sld_kernel)
+against the generic kernels they replace (MGB_NO_RKD=1 / MGB_NO_SLD=1, read
+once per process: the generic runs are subprocesses)."""
 import json
 import os
 import subprocess
@@ -29,7 +30,11 @@ print(json.dumps(out))
 """
 
 CASES = [("sdirk", 3, 4.0, 512, 256, 4, "v_cycle"), ("sdirk", 3, 4.0, 4096, 64, 4, "two_level"),
-         ("sdirk", 2, 2.0, 1024, 128, 4, "v_cycle"), ("sdirk", 1, 3.0, 512, 64, 2, "two_level")]
+         ("sdirk", 2, 2.0, 1024, 128, 4, "v_cycle"), ("sdirk", 1, 3.0, 512, 64, 2, "two_level"),
+         # direct-corrected coarse operators: ERK two-level (cfg1's scheme), SDIRK V-cycles whose
+         # deep levels have slow-decaying factors (hierarchical scan)
+         ("erk", 1, 0.85, 1024, 256, 8, "two_level"), ("erk", 3, 0.85, 512, 128, 4, "two_level"),
+         ("sdirk", 3, 4.0, 1024, 1024, 4, "v_cycle")]
 
 
 def _run(env_extra):
@@ -41,9 +46,9 @@ def _run(env_extra):
 
 
 @pytest.mark.gpu
-def test_dedicated_sdirk_kernel_bitwise_equals_generic_kernel():
+def test_dedicated_kernels_bitwise_equal_generic_kernels():
     new = _run({})
-    old = _run({"MGB_NO_RKD": "1"})
+    old = _run({"MGB_NO_RKD": "1", "MGB_NO_SLD": "1"})
     assert new.keys() == old.keys()
     for k in new:
         assert new[k]["norms"] == old[k]["norms"], k
