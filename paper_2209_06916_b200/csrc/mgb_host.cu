@@ -1002,8 +1002,10 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
       if (tn.c1_c && v.C != tn.c1_c) return false;
       if (tn.c1_no_occ2 && v.occ == 2) return false;
       // wide segments (cluster sizes 1-2 on 4096-point rows) measured slower than
-      // the single-CTA kernel for many-interval levels: opt-in only
-      if (v.P >= 4 && !tn.c1_wide && !tn.c1_c) return false;
+      // the single-CTA kernel for many-interval levels: opt-in only -- except on rows
+      // too long for the single-CTA kernel (n_x = 16384), where they are the only way
+      // to run many intervals at once (cfg5 proxy 16384 x 16384: 970 -> 608 ms)
+      if (v.P >= 4 && !tn.c1_wide && !tn.c1_c && st->fn) return false;
       return true;
     };
     const ClusterVariant* best = nullptr;
