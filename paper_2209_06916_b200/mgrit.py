@@ -19,6 +19,15 @@ Kernel schedule of one cycle on a level with nu = 1:
 Skipping interior F-point writes in FC/FR is exact: only u_{km+m-1} is read
 before the closing F-relaxation rewrites every F-point (verified
 bitwise on the reference).
+
+Opening F-relaxation of iterations >= 2 (fine level): the closing F-relaxation
+of iteration k (CF pass, mgrit.py:247) leaves u_{km+j} = Phi^j u_{km}; the
+opening F-relaxation of iteration k+1 (mgrit.py:231) recomputes exactly those
+values from the same C-points with the same kernel, so the solve loop replaces
+it by a read of the stored u_{km+m-1}: the first FC (nu = 0: FR) pass is then
+one C-step (residual step) per interval instead of m steps.  Bitwise the same
+iterate and history (``ELIDE_OPENING_F_RELAX = False`` runs the full pass;
+tests/test_gpu_parity.py compares both).
 """
 
 from __future__ import annotations
@@ -37,6 +46,9 @@ from .device import device_sum, is_tensor, plan_for, ptr, require_cuda, stream_h
 nat_load, nat_check = _native.load, _native.check
 #: tests: fill the rows ``MgritSolver._upload`` does not copy with NaN
 POISON_SKIPPED_ROWS = False
+#: iterations >= 2 of ``solve`` read the F-points the previous closing F-relaxation left
+#: instead of recomputing them (module docstring); False: recompute like the reference
+ELIDE_OPENING_F_RELAX = True
 from .stepping import Stepper
 
 _F64 = 8
@@ -311,7 +323,10 @@ class MgritSolver:
         return out
 
     def _cycle(self, l: int, u: int, g: Optional[int], u_zero: bool, want_norm: bool,
-               kind: Optional[str] = None, pre_cf=None) -> None:
+               kind: Optional[str] = None, pre_cf=None, f_relaxed: bool = False) -> None:
+        """One cycle on level ``l``.  ``f_relaxed``: the F-points of ``u`` are the
+        F-relaxation of its C-points (the state a previous cycle's CF pass left),
+        so the opening F-relaxation reads u_{km+m-1} instead of recomputing it."""
         cfg = self.config
         kind = kind or cfg.cycle
         L = self.levels[l]
@@ -321,10 +336,15 @@ class MgritSolver:
         zero = ptr(self.zero_row)
         u0row = zero if u_zero else u
         src, stride = (None if u_zero else u), m * n
+        f_relaxed = f_relaxed and not u_zero and ELIDE_OPENING_F_RELAX
         for i in range(cfg.nu):
             dst = L.cbuf[i % 2]
-            self._timed(f"L{l}.FC", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
-                        c_src0=u0row, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g)
+            if i == 0 and f_relaxed:  # C-step from the stored last F-point of every interval
+                self._timed(f"L{l}.FC", plan.relax, nI, m, 0, c_src=u + (m - 1) * row,
+                            c_stride=m * n, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g)
+            else:
+                self._timed(f"L{l}.FC", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
+                            c_src0=u0row, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g)
             src, stride = ptr(dst), n
         gC = self.gcoarse[l + 1]
         uC = self.ucoarse[l + 1]
@@ -332,9 +352,14 @@ class MgritSolver:
             cref, cref_stride = (zero, 0) if u_zero else (u + m * row, m * n)
         else:
             cref, cref_stride = src + row, n
-        self._timed(f"L{l}.FR", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
-                    c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
-                    tail_out=ptr(gC) + row, tail_stride=n, g=g)
+        if cfg.nu == 0 and f_relaxed:  # residual step from the stored last F-points
+            self._timed(f"L{l}.FR", plan.relax, nI, m, 0, c_src=u + (m - 1) * row, c_stride=m * n,
+                        tail=2, cref=cref, cref_stride=cref_stride,
+                        tail_out=ptr(gC) + row, tail_stride=n, g=g)
+        else:
+            self._timed(f"L{l}.FR", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
+                        c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
+                        tail_out=ptr(gC) + row, tail_stride=n, g=g)
         self._coarse_solve(l + 1, kind)
         if pre_cf is not None:  # last reader of the incoming F-points (solve's initial norm)
             pre_cf()
@@ -436,7 +461,7 @@ class MgritSolver:
         converged = False
         it = 0
         while it < cfg.max_iters:
-            self._cycle(0, up, None, False, True, pre_cf=hook)
+            self._cycle(0, up, None, False, True, pre_cf=hook, f_relaxed=it > 0)
             it += 1
             if hook is not None:
                 hook = None
@@ -561,13 +586,13 @@ def solve_many(jobs, streams: Optional[int] = 8, graphs: bool = True,
                        bytes=8.0 * (problem.n_t + 1) * problem.n_x, norms=[], it=0,
                        converged=False, ev=torch.cuda.Event(), wall=0.0, graph=None))
 
-    def enqueue(k, first):
+    def enqueue(k, first, f_relaxed=True):
         d = st[k]
         sol = d["sol"]
         if first:
             sol._residual_partials(d["up"], None)
         else:
-            sol._cycle(0, d["up"], None, False, True)
+            sol._cycle(0, d["up"], None, False, True, f_relaxed=f_relaxed)
         device_sum(ptr(sol.partials), sol.levels[0].n_int, ptr(sol.sumbuf))
         host[k:k + 1].copy_(sol.sumbuf, non_blocking=True)
 
@@ -597,7 +622,9 @@ def solve_many(jobs, streams: Optional[int] = 8, graphs: bool = True,
     def next_cycle(k):
         d = st[k]
         with torch.cuda.stream(d["stream"]):
-            if d["graph"] is not None:
+            if d["it"] == 1:  # the first cycle starts from an arbitrary iterate: full opening pass
+                enqueue(k, False, f_relaxed=False)
+            elif d["graph"] is not None:
                 d["graph"].replay()
             else:
                 enqueue(k, False)

@@ -464,3 +464,28 @@ def test_single_cta_gmres_every_stencil_width(extra_env):
     r = subprocess.run([sys.executable, "-c", _SINGLE_CTA_CHECK.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+# ------------------------------------- opening F-relaxation of iterations >= 2
+
+@pytest.mark.parametrize("fam,p,c,n_x,n_t,m,cyc,nu", [
+    ("erk", 3, 0.85, 256, 1024, 8, "v_cycle", 1), ("erk", 1, 0.85, 128, 256, 4, "two_level", 0),
+    ("erk", 3, 0.85, 128, 1024, 4, "f_cycle", 2), ("sdirk", 3, 4.0, 512, 256, 4, "v_cycle", 1),
+    ("erk", 5, 0.85, 4096, 256, 16, "two_level", 1), ("sdirk", 3, 4.0, 256, 256, 4, "two_level", 0)])
+def test_elided_opening_f_relaxation_is_bitwise_the_full_pass(fam, p, c, n_x, n_t, m, cyc, nu,
+                                                              monkeypatch):
+    """Iterations >= 2 of solve() read the F-points the previous closing
+    F-relaxation left instead of recomputing them (mgrit.py:231 vs :247): same
+    iterate and history, bit for bit, as the reference-style full pass."""
+    from paper_2209_06916_b200 import mgrit as M
+    spec = P.DiscretizationSpec(fam, p, c, n_x, n_t)
+    prob = P.experiments.build_problem(spec, m, "v_cycle" if cyc == "f_cycle" else cyc)
+    cfg = P.MgritConfig(cycle=cyc, nu=nu, max_iters=6)
+    u_a = P.MgritSolver(prob, cfg).initial_state()
+    u_b = u_a.copy()
+    rep_a = P.solve(prob, cfg, initial_iterate=u_a)
+    monkeypatch.setattr(M, "ELIDE_OPENING_F_RELAX", False)
+    rep_b = P.solve(prob, cfg, initial_iterate=u_b)
+    assert rep_a.iterations == rep_b.iterations >= 2
+    assert rep_a.residual_norms == rep_b.residual_norms
+    assert np.array_equal(u_a, u_b)
