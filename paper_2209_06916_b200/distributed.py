@@ -167,14 +167,23 @@ class GpuEngine(Engine):
             return (None if u_zero else self._p(u)), m * n, u0row
         return self._p(src), n, u0row
 
-    def fc(self, l, u, g, src, cb, k0, nb, u_zero):
+    #: iterations >= 2: the opening F-relaxation reads the stored last F-points
+    #: (MgritSolver._cycle, mgrit.py module docstring)
+    supports_f_relaxed = True
+
+    def fc(self, l, u, g, src, cb, k0, nb, u_zero, f_relaxed=False):
         m, n = self.m[l], self.n
+        if f_relaxed and src is None and not u_zero:
+            self._relax(f"L{l}.FC", l, nb, m, 0, k_global0=k0, c_src=self._p(u, m - 1),
+                        c_stride=m * n, tail=1, tail_out=self._p(cb, 1), tail_stride=n,
+                        g=self._p(g))
+            return
         c_src, stride, u0row = self._src(l, u, src, u_zero)
         self._relax(f"L{l}.FC", l, nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
                     c_src0=u0row, tail=1, tail_out=self._p(cb, 1), tail_stride=n,
                     g=self._p(g))
 
-    def fr(self, l, u, g, src, gn, k0, nb, u_zero):
+    def fr(self, l, u, g, src, gn, k0, nb, u_zero, f_relaxed=False):
         m, n = self.m[l], self.n
         c_src, stride, u0row = self._src(l, u, src, u_zero)
         if src is None:
@@ -182,6 +191,11 @@ class GpuEngine(Engine):
                                  else (self._p(u, m), m * n))
         else:
             cref, cref_stride = self._p(src, 1), n
+        if f_relaxed and src is None and not u_zero:
+            self._relax(f"L{l}.FR", l, nb, m, 0, k_global0=k0, c_src=self._p(u, m - 1),
+                        c_stride=m * n, tail=2, cref=cref, cref_stride=cref_stride,
+                        tail_out=self._p(gn, 1), tail_stride=n, g=self._p(g))
+            return
         self._relax(f"L{l}.FR", l, nb, m, m - 1, k_global0=k0, c_src=c_src, c_stride=stride,
                     c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
                     tail_out=self._p(gn, 1), tail_stride=n, g=self._p(g))
@@ -320,19 +334,22 @@ class ShardedMgritSolver:
         return eng.from_comm(e_t, None)
 
     # --------------------------------------------------------------- cycle
-    def _cycle(self, l, u, g, u_zero, want_norm, kind):
+    def _cycle(self, l, u, g, u_zero, want_norm, kind, f_relaxed=False):
         """One cycle on sharded level l (mgrit.py:225-247, MgritSolver._cycle)."""
+        from . import mgrit as _mg
         eng, cfg = self.engine, self.config
         k0, nb = self.blocks[l]
         bufs = self._buffers()
         src = None
+        opt = ({"f_relaxed": True} if f_relaxed and not u_zero and _mg.ELIDE_OPENING_F_RELAX
+               and getattr(eng, "supports_f_relaxed", False) else {})
         for i in range(cfg.nu):
             cb = bufs["cb"][l][i % 2]
-            eng.fc(l, u, g, src, cb, k0, nb, u_zero)
+            eng.fc(l, u, g, src, cb, k0, nb, u_zero, **(opt if i == 0 else {}))
             self._pass_right(cb, nb)
             src = cb
         gn, e = bufs["g"][l + 1], bufs["u"][l + 1]
-        eng.fr(l, u, g, src, gn, k0, nb, u_zero)
+        eng.fr(l, u, g, src, gn, k0, nb, u_zero, **(opt if cfg.nu == 0 else {}))
         e = self._coarse(l + 1, e, gn, nb, kind)
         return eng.cf(l, u, g, src, e, k0, nb, u_zero, want_norm)
 
@@ -370,9 +387,11 @@ class ShardedMgritSolver:
             dist.broadcast(tot, src=0, group=self.group)
         return math.sqrt(float(tot.item()))
 
-    def iterate(self, u_loc):
-        """One cycle on the local block; returns the level-0 norm partials."""
-        return self._cycle(0, u_loc, None, False, True, self.config.cycle)
+    def iterate(self, u_loc, f_relaxed=False):
+        """One cycle on the local block; returns the level-0 norm partials.
+        ``f_relaxed``: the F-points are the F-relaxation of the C-points (the
+        state the previous cycle left)."""
+        return self._cycle(0, u_loc, None, False, True, self.config.cycle, f_relaxed)
 
     def solve(self, u_loc) -> SolveReport:
         """Run to the halting rule; every rank returns the same report."""
@@ -381,7 +400,7 @@ class ShardedMgritSolver:
         norms = [self._global_sum(self.engine.initial_partials(u_loc, self.nb))]
         it, converged = 0, False
         while it < cfg.max_iters:
-            part = self.iterate(u_loc)
+            part = self.iterate(u_loc, f_relaxed=it > 0)
             it += 1
             norms.append(self._global_sum(part))
             if norms[0] > 0 and norms[-1] / norms[0] <= cfg.tol:
