@@ -360,7 +360,7 @@ class ShardedMgritSolver:
         # from e = 0: the passes never read e (zero C-points), CF writes all of it
         if kind == "f_cycle":
             self._cycle(child, e, gn, True, False, "f_cycle")
-            self._cycle(child, e, gn, False, False, "v_cycle")
+            self._cycle(child, e, gn, False, False, "v_cycle", f_relaxed=True)
         else:
             self._cycle(child, e, gn, True, False, "v_cycle")
         return e

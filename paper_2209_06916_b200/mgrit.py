@@ -392,7 +392,8 @@ class MgritSolver:
                         ptr(gC), self.problem.points_on_level(child))
         elif kind == "f_cycle":
             self._cycle(child, ptr(uC), ptr(gC), True, False, "f_cycle")
-            self._cycle(child, ptr(uC), ptr(gC), False, False, "v_cycle")
+            # the V-cycle starts from the F-cycle's result, whose F-points its CF pass relaxed
+            self._cycle(child, ptr(uC), ptr(gC), False, False, "v_cycle", f_relaxed=True)
         else:
             self._cycle(child, ptr(uC), ptr(gC), True, False, "v_cycle")
 

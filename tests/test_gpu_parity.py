@@ -471,7 +471,11 @@ def test_single_cta_gmres_every_stencil_width(extra_env):
 @pytest.mark.parametrize("fam,p,c,n_x,n_t,m,cyc,nu", [
     ("erk", 3, 0.85, 256, 1024, 8, "v_cycle", 1), ("erk", 1, 0.85, 128, 256, 4, "two_level", 0),
     ("erk", 3, 0.85, 128, 1024, 4, "f_cycle", 2), ("sdirk", 3, 4.0, 512, 256, 4, "v_cycle", 1),
-    ("erk", 5, 0.85, 4096, 256, 16, "two_level", 1), ("sdirk", 3, 4.0, 256, 256, 4, "two_level", 0)])
+    ("erk", 5, 0.85, 4096, 256, 16, "two_level", 1), ("sdirk", 3, 4.0, 256, 256, 4, "two_level", 0),
+    # F-cycles: the V-cycle after each level's F-cycle also starts from relaxed F-points
+    # (GMRES-corrected coarse levels on the single-CTA and cluster kernels)
+    ("erk", 3, 0.85, 256, 4096, 4, "f_cycle", 1), ("erk", 3, 0.85, 4096, 512, 8, "f_cycle", 1),
+    ("sdirk", 3, 4.0, 512, 1024, 4, "f_cycle", 1)])
 def test_elided_opening_f_relaxation_is_bitwise_the_full_pass(fam, p, c, n_x, n_t, m, cyc, nu,
                                                               monkeypatch):
     """Iterations >= 2 of solve() read the F-points the previous closing
