@@ -156,7 +156,7 @@ class ClockSampler:
                 "source": "nvml 5 ms" if self._nvml is not None else "nvidia-smi"}
 
 
-def pass_work(cf, level, n_int, m, prog, kind):
+def pass_work(cf, level, n_int, m, prog, kind, steps=None):
     """(algorithmic FP64 flops, algorithmic HBM bytes) of one launch of a fine
     explicit-stencil pass over ``n_int`` intervals:
       FC: m steps per interval (m-1 F + the C step): reads the C-point row,
@@ -181,7 +181,7 @@ def pass_work(cf, level, n_int, m, prog, kind):
         per_pt = 2.0 * taps
     else:
         return None, None
-    flops = per_pt * n * n_int * m
+    flops = per_pt * n * n_int * (m if steps is None else steps)
     rows = {"FC": 2 * n_int, "FR": 3 * n_int, "CF": n_int * m + 1 + 2 * (n_int + 1)}[kind]
     return flops, 8.0 * n * rows
 
@@ -202,6 +202,8 @@ def rooflines(cf, prob, passes, total_ms, n_int0, fp64_peak):
     bound is whichever of HBM bytes / peak and FP64 flops / issue bound is
     larger.  Exact mode issues DMUL + DADD per tap, so its FP64 issue bound is
     half the DFMA peak (reported as ``frac_of_issue_bound``)."""
+    from paper_2209_06916_b200 import mgrit as _mg
+    elided = bool(_mg.ELIDE_OPENING_F_RELAX)
     hbm_peak, peak_kind = peaks()
     prog = prob.steppers[0].program
     out = {}
@@ -209,10 +211,14 @@ def rooflines(cf, prob, passes, total_ms, n_int0, fp64_peak):
         name = f"L0.{kind}"
         if name not in passes:
             continue
-        flops, nbytes = pass_work(cf, 0, n_int0, prob.m[0], prog, kind)
+        cnt, ms = passes[name]
+        # the opening FC pass of iterations >= 2 is one C-step per interval from the stored
+        # last F-point (mgrit.ELIDE_OPENING_F_RELAX): average steps per launch of the solve
+        m0 = prob.m[0]
+        steps = (m0 + (cnt - 1)) / cnt if (kind == "FC" and elided and cnt > 1) else None
+        flops, nbytes = pass_work(cf, 0, n_int0, m0, prog, kind, steps)
         if flops is None:
             continue
-        cnt, ms = passes[name]
         t = ms / cnt / 1e3
         # exact explicit stencils issue DMUL + DADD per tap; staged RK mixes fused solves
         # with exact stencil / tableau sums and is reported against the DFMA peak
@@ -230,6 +236,8 @@ def rooflines(cf, prob, passes, total_ms, n_int0, fp64_peak):
             ach = nbytes / t / 1e9
             r = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                  "frac": round(ach / hbm_peak, 4), "peak_source": peak_kind + " (MEASURED_PEAKS.json)"}
+        if steps is not None:
+            r["steps_per_launch_avg"] = round(steps, 3)
         r.update({"kernel": f"relax kernel {name}", "algorithmic_bytes": nbytes,
                   "launch_ms": round(t * 1e3, 4), "traffic": traffic, "traffic_source": tsrc,
                   "share_of_step": round(ms / total_ms, 4)})
