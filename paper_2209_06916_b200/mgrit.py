@@ -607,8 +607,10 @@ def solve_many(jobs, streams: Optional[int] = 8, graphs: bool = True,
             u = sol.initial_state() if d["init"] is None else d["init"]
             d["ud"], d["uh"] = to_device(u)
             d["up"] = ptr(d["ud"])
-            if graphs:
-                for plan in [L.plan for L in sol.levels] + sol.plans:
+            plans = [L.plan for L in sol.levels] + sol.plans
+            # user callables (device.CallablePlan) run arbitrary torch code: not captured
+            if graphs and not any(getattr(pl.prog, "kind", "") == "callable" for pl in plans):
+                for plan in plans:
                     plan.reserve()
                 g = torch.cuda.CUDAGraph()
                 g.capture_begin(capture_error_mode="thread_local")
