@@ -1968,10 +1968,11 @@ __device__ __forceinline__ void win_step(const double* __restrict__ src, double*
                                          const double (&wd)[SPAN + 1], double* __restrict__ gdst, int n, int nthr,
                                          bool own) {
   // outputs per pass (window of H + SPAN in registers)
-  // (4 measured fastest on B200 for spans 9 and 30 at 16 points per thread: 8 and 16
-  // trade fewer shared loads for register spills)
+  // (2 measured fastest on B200 for spans 9 and 30 at 16 points per thread -- cfg4 fine
+  // FR / CF 2.16 / 2.34 ms vs 2.26 / 2.44 at 4 and 2.29 / 2.50 at 8: wider parts trade
+  // fewer shared loads for registers the FP64 chains need)
 #ifndef MGB_WIN_H
-#define MGB_WIN_H 4
+#define MGB_WIN_H 2
 #endif
   constexpr int H = MGB_WIN_H < P ? MGB_WIN_H : P;
   static_assert(TT == 0 || (P - 1 + P - 1 + SPAN) / P < WIN_X, "wrap replica too narrow");
