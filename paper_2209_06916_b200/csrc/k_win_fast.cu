@@ -1,6 +1,10 @@
 // Register-window stencil relaxation, fast mode (DFMA).
 #include "mgb_registry.h"
 
+#ifndef MGB_WIN_MINB256
+#define MGB_WIN_MINB256 2  // CTAs per SM of the 256-thread fixed-geometry build
+#endif
+
 namespace mgb {
 // key nst = 1: dedicated double-buffered kernel at <= 256 threads, 2 CTAs/SM;
 // nst = 2: generic single-buffer slice kernel (fallback: odd n_x, 16384-point rows)
@@ -14,7 +18,7 @@ namespace mgb {
   register_kernel(KernelKey{K_WIN, 16, SPAN, 3, 0},                                             \
                   reinterpret_cast<const void*>(&relax_win_kernel<16, SPAN, false, 512, 1, 512>)); \
   register_kernel(KernelKey{K_WIN, 16, SPAN, 4, 0},                                             \
-                  reinterpret_cast<const void*>(&relax_win_kernel<16, SPAN, false, 256, 2, 256>));
+                  reinterpret_cast<const void*>(&relax_win_kernel<16, SPAN, false, 256, MGB_WIN_MINB256, 256>));
 #define WIN_P(P) \
   WIN_D(P, 1) WIN_D(P, 2) WIN_D(P, 3) WIN_D(P, 4) WIN_D(P, 5) WIN_D(P, 9) WIN_D(P, 16) WIN_D(P, 30)
 void register_win_fast() {
