@@ -220,7 +220,7 @@ def test_full_size_reference_runs_recorded():
     """Every full-size / proxy reference run has the reference's histories.json
     iteration count, and the full-size runs repeat histories.json's history
     (to the last bits: those runs used a multithreaded BLAS ddot in the norm)."""
-    for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg4p", "cfg5p"):
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg4p", "cfg5p", "cfg5q"):
         path = os.path.join(HERE, "full", name + ".json")
         if not os.path.exists(path):
             continue
