@@ -28,6 +28,17 @@ it by a read of the stored u_{km+m-1}: the first FC (nu = 0: FR) pass is then
 one C-step (residual step) per interval instead of m steps.  Bitwise the same
 iterate and history (``ELIDE_OPENING_F_RELAX = False`` runs the full pass;
 tests/test_gpu_parity.py compares both).
+
+First interval of a coarse level (nu >= 1): the error at t = 0 is zero, so on
+levels >= 1 interval 0 starts from the same zero C-point in the FC, FR and CF
+passes of a cycle (mgrit.py:231-247): the FR pass recomputes the FC pass's
+F-points and gets r_1 = (g + Phi u_{m-1}) - (Phi u_{m-1} + g) = 0 exactly, the
+child level then returns e_1 = 0, and the CF pass recomputes the same F-points
+once more.  The FC pass therefore writes its F-points, the FR / CF passes run on
+intervals 1.. only and r_1 is set to zero -- on a single-interval level (cfg4's
+level 3) two of the three passes disappear, and a 16-interval level (cfg4's
+level 2) fits one wave of clusters.  Bitwise the same iterate and history
+(``ELIDE_FIRST_INTERVAL = False`` recomputes).
 """
 
 from __future__ import annotations
@@ -49,6 +60,9 @@ POISON_SKIPPED_ROWS = False
 #: iterations >= 2 of ``solve`` read the F-points the previous closing F-relaxation left
 #: instead of recomputing them (module docstring); False: recompute like the reference
 ELIDE_OPENING_F_RELAX = True
+#: coarse levels: the first interval starts from e_0 = 0 in every pass, so its FR and CF
+#: work repeats the FC pass bit for bit (module docstring); False: recompute
+ELIDE_FIRST_INTERVAL = True
 from .stepping import Stepper
 
 _F64 = 8
@@ -337,11 +351,18 @@ class MgritSolver:
         u0row = zero if u_zero else u
         src, stride = (None if u_zero else u), m * n
         f_relaxed = f_relaxed and not u_zero and ELIDE_OPENING_F_RELAX
+        # coarse levels: interval 0 repeats the FC pass in FR and CF (module docstring)
+        skip0 = ELIDE_FIRST_INTERVAL and l >= 1 and cfg.nu >= 1
+        k0 = 1 if skip0 else 0
         for i in range(cfg.nu):
             dst = L.cbuf[i % 2]
             if i == 0 and f_relaxed:  # C-step from the stored last F-point of every interval
                 self._timed(f"L{l}.FC", plan.relax, nI, m, 0, c_src=u + (m - 1) * row,
                             c_stride=m * n, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g)
+            elif i == 0 and skip0 and u_zero:  # interval 0's F-points are final: written here
+                self._timed(f"L{l}.FC", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
+                            c_src0=u0row, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g,
+                            u=u, write_f=2)
             else:
                 self._timed(f"L{l}.FC", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
                             c_src0=u0row, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g)
@@ -352,10 +373,18 @@ class MgritSolver:
             cref, cref_stride = (zero, 0) if u_zero else (u + m * row, m * n)
         else:
             cref, cref_stride = src + row, n
+        g_k0 = None if g is None else g + k0 * m * row
         if cfg.nu == 0 and f_relaxed:  # residual step from the stored last F-points
             self._timed(f"L{l}.FR", plan.relax, nI, m, 0, c_src=u + (m - 1) * row, c_stride=m * n,
                         tail=2, cref=cref, cref_stride=cref_stride,
                         tail_out=ptr(gC) + row, tail_stride=n, g=g)
+        elif skip0:
+            gC[1].zero_()  # r_1 = 0 exactly
+            if nI > 1:
+                self._timed(f"L{l}.FR", plan.relax, nI - 1, m, m - 1, k_global0=1,
+                            c_src=src + stride * _F64, c_stride=stride, tail=2,
+                            cref=cref + cref_stride * _F64, cref_stride=cref_stride,
+                            tail_out=ptr(gC) + 2 * row, tail_stride=n, g=g_k0)
         else:
             self._timed(f"L{l}.FR", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
                         c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
@@ -368,13 +397,23 @@ class MgritSolver:
             c_src, c_stride = (None if u_zero else u), m * n
         else:
             c_src, c_stride = src, n
-        self._timed(f"L{l}.CF", plan.relax, nI, m, m - 1, c_src=c_src, c_stride=c_stride,
-                    c_src0=u0row, e=ptr(uC),
-                   e_stride=n, c_out=u, c_out_stride=m * n, c_last_out=u + nI * m * row,
-                   u=u, write_f=2, g=g,
-                   tail=2 if fuse_norm else 0, cref=(c_src + row) if fuse_norm else None,
-                   cref_stride=n, cref_e=ptr(uC) + row, cref_e_stride=n,
-                   partials=ptr(self.partials) if fuse_norm else None)
+        if skip0:
+            if nI > 1:
+                self._timed(f"L{l}.CF", plan.relax, nI - 1, m, m - 1, k_global0=1,
+                            c_src=c_src + c_stride * _F64, c_stride=c_stride,
+                            e=ptr(uC) + row, e_stride=n, c_out=u + m * row, c_out_stride=m * n,
+                            c_last_out=u + nI * m * row, u=u + m * row, write_f=2, g=g_k0)
+            else:  # the level's last C-point: C-relaxed value + correction (mgrit.py:246)
+                torch = self._torch
+                torch.add(L.cbuf[(cfg.nu - 1) % 2][1], uC[1], out=self.ucoarse[l][m])
+        else:
+            self._timed(f"L{l}.CF", plan.relax, nI, m, m - 1, c_src=c_src, c_stride=c_stride,
+                        c_src0=u0row, e=ptr(uC),
+                        e_stride=n, c_out=u, c_out_stride=m * n, c_last_out=u + nI * m * row,
+                        u=u, write_f=2, g=g,
+                        tail=2 if fuse_norm else 0, cref=(c_src + row) if fuse_norm else None,
+                        cref_stride=n, cref_e=ptr(uC) + row, cref_e_stride=n,
+                        partials=ptr(self.partials) if fuse_norm else None)
         if want_norm and not fuse_norm:
             self._timed("L0.R", self._residual_partials, u, g)
 
