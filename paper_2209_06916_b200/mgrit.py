@@ -296,6 +296,8 @@ class MgritSolver:
             self.ucoarse.append(torch.zeros((npts, n_x), dtype=torch.float64, device="cuda"))
             self.gcoarse.append(torch.zeros((npts, n_x), dtype=torch.float64, device="cuda"))
         self.plans = [plan_for(s.program, self.plan_tag) for s in pr.steppers]
+        #: gcoarse[l][1] (r_1 of level l - 1) still holds its zeros (ELIDE_FIRST_INTERVAL)
+        self._r1_zero = [True] * (nlev + 2)
         self.zero_row = torch.zeros(n_x, dtype=torch.float64, device="cuda")
         n0 = self.levels[0].n_int
         self.partials = torch.empty(max(n0, 1), dtype=torch.float64, device="cuda")
@@ -375,17 +377,21 @@ class MgritSolver:
             cref, cref_stride = src + row, n
         g_k0 = None if g is None else g + k0 * m * row
         if cfg.nu == 0 and f_relaxed:  # residual step from the stored last F-points
+            self._r1_zero[l + 1] = False
             self._timed(f"L{l}.FR", plan.relax, nI, m, 0, c_src=u + (m - 1) * row, c_stride=m * n,
                         tail=2, cref=cref, cref_stride=cref_stride,
                         tail_out=ptr(gC) + row, tail_stride=n, g=g)
         elif skip0:
-            gC[1].zero_()  # r_1 = 0 exactly
+            if not self._r1_zero[l + 1]:  # r_1 = 0 exactly: the row is zero from allocation on
+                gC[1].zero_()             # unless a full FR pass of this solver wrote it
+                self._r1_zero[l + 1] = True
             if nI > 1:
                 self._timed(f"L{l}.FR", plan.relax, nI - 1, m, m - 1, k_global0=1,
                             c_src=src + stride * _F64, c_stride=stride, tail=2,
                             cref=cref + cref_stride * _F64, cref_stride=cref_stride,
                             tail_out=ptr(gC) + 2 * row, tail_stride=n, g=g_k0)
         else:
+            self._r1_zero[l + 1] = False
             self._timed(f"L{l}.FR", plan.relax, nI, m, m - 1, c_src=src, c_stride=stride,
                         c_src0=u0row, tail=2, cref=cref, cref_stride=cref_stride,
                         tail_out=ptr(gC) + row, tail_stride=n, g=g)
