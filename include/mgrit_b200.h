@@ -118,6 +118,11 @@ typedef struct {
   double* partials;     /* per-interval sum of squares of the residual row   */
   int32_t* stats_depth; /* SL_GMRES: per-interval GMRES depth of the last solve */
   double* stats_res;    /* SL_GMRES: per-interval relative residual          */
+  double* z_out;        /* tail == 2, explicit / staged-RK plans: also store the
+                           tail step's value g + Phi u_last (the residual before
+                           cref is subtracted) at z_out + k*z_stride: the C-relaxed
+                           value c_relax would compute next (mgrit.py:148-149) */
+  int64_t z_stride;
 } mgb_relax_args;
 
 int mgb_relax(mgb_step* step, const mgb_relax_args* args, void* stream);

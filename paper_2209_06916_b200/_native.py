@@ -48,6 +48,7 @@ class RelaxArgs(ctypes.Structure):
         ("cref_e", ctypes.c_void_p), ("cref_e_stride", _i64),
         ("partials", ctypes.c_void_p),
         ("stats_depth", ctypes.c_void_p), ("stats_res", ctypes.c_void_p),
+        ("z_out", ctypes.c_void_p), ("z_stride", ctypes.c_int64),
     ]
 
 

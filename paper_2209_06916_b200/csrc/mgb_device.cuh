@@ -1274,6 +1274,7 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_kernel(const StepParams* __r
 #pragma unroll
             for (int q = 0; q < P; ++q) r[q] = y[q];
           }
+          if (a.z_out) store_chunk<P>(a.z_out + k * a.z_stride, t, r);  // g + Phi u_last
           double cr[P];
           load_chunk<P>(a.cref + k * a.cref_stride, t, cr);
           if (a.cref_e) {
@@ -1580,6 +1581,7 @@ __global__ void __launch_bounds__(512, MGB_RKD_MINB) relax_rkd_kernel(const Step
 #pragma unroll
             for (int q = 0; q < P; ++q) rr[q] = y[q];
           }
+          if (a.z_out) store_chunk<P>(a.z_out + k * a.z_stride, t, rr);  // g + Phi u_last
           double cr[P];
           load_chunk<P>(a.cref + k * a.cref_stride, t, cr);
           if (a.cref_e) {
@@ -2162,6 +2164,7 @@ __global__ void __launch_bounds__(MAXT, MINB) relax_win_kernel(const StepParams*
             z.x = __dadd_rn(gv[u].x, z.x);  // g + Phi u (commutative: bitwise either order)
             z.y = __dadd_rn(gv[u].y, z.y);
           }
+          if (a.tail == 2 && a.z_out) *reinterpret_cast<double2*>(a.z_out + k * a.z_stride + i) = z;
           if (a.tail == 1) {  // C-relaxation (mgrit.py:148-149)
             *reinterpret_cast<double2*>(a.tail_out + k * a.tail_stride + i) = z;
           } else {  // residual (g + Phi u) - u_C (mgrit.py:159-161)

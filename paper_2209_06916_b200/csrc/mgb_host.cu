@@ -438,6 +438,7 @@ mgb_relax_args sub_range(const mgb_relax_args& a, long long k0, long long cnt, i
   if (s.tail_out) s.tail_out += k0 * a.tail_stride;
   if (s.cref) s.cref += k0 * a.cref_stride;
   if (s.cref_e) s.cref_e += k0 * a.cref_e_stride;
+  if (s.z_out) s.z_out += k0 * a.z_stride;
   if (s.partials) s.partials += k0;
   if (s.stats_depth) s.stats_depth += k0;
   if (s.stats_res) s.stats_res += k0;
@@ -967,10 +968,14 @@ int mgb_relax(mgb_step* st, const mgb_relax_args* a, void* stream) {
   if (a->tail == 1 && !a->tail_out) return fail(MGB_ERR_INVALID, "C-relax tail needs tail_out");
   if (a->tail == 2 && !a->cref) return fail(MGB_ERR_INVALID, "residual tail needs cref");
   if (a->write_f && !a->u) return fail(MGB_ERR_INVALID, "write_f needs u");
+  if (a->z_out && (a->tail != 2 || !(st->dkind == mgb::K_WIN || st->dkind == mgb::K_GEN ||
+                                      (st->dkind == mgb::K_RK))))
+    return fail(MGB_ERR_UNSUPPORTED, "z_out needs a residual tail on an explicit or staged-RK plan");
   if (st->vec16) {  // dedicated stencil kernel moves rows with 16-byte accesses
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     const bool ok = al(a->c_src) && al(a->c_src0) && al(a->e) && al(a->c_out) && al(a->c_last_out) &&
-                    al(a->u) && al(a->g) && al(a->tail_out) && al(a->cref) && al(a->cref_e) &&
+                    al(a->u) && al(a->g) && al(a->tail_out) && al(a->cref) && al(a->cref_e) && al(a->z_out) &&
+                    a->z_stride % 2 == 0 &&
                     a->c_stride % 2 == 0 && a->e_stride % 2 == 0 && a->c_out_stride % 2 == 0 &&
                     a->tail_stride % 2 == 0 && a->cref_stride % 2 == 0 && a->cref_e_stride % 2 == 0;
     if (!ok) return fail(MGB_ERR_INVALID, "explicit-stencil relax needs 16-byte aligned rows and even strides");

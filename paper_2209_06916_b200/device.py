@@ -184,7 +184,8 @@ class StepPlan:
               c_out=None, c_out_stride: int = 0, c_last_out=None, u=None, write_f: int = 0, g=None,
               tail: int = 0, tail_out=None, tail_stride: int = 0, cref=None,
               cref_stride: int = 0, cref_e=None, cref_e_stride: int = 0, partials=None,
-              stats_depth=None, stats_res=None, stream=None) -> None:
+              stats_depth=None, stats_res=None, z_out=None, z_stride: int = 0,
+              stream=None) -> None:
         """Launch one interval relaxation (see ``mgb_relax_args``).  Pointer
         arguments are ints (device addresses) or None."""
         a = nat.RelaxArgs()
@@ -196,6 +197,7 @@ class StepPlan:
         a.tail_out, a.tail_stride = tail_out, tail_stride
         a.cref, a.cref_stride, a.cref_e, a.cref_e_stride = cref, cref_stride, cref_e, cref_e_stride
         a.partials, a.stats_depth, a.stats_res = partials, stats_depth, stats_res
+        a.z_out, a.z_stride = z_out, z_stride
         nat.check(self._lib.mgb_relax(self._h, ctypes.byref(a),
                                       stream if stream is not None else stream_handle()))
 
@@ -245,7 +247,8 @@ class CallablePlan:
               c_out=None, c_out_stride: int = 0, c_last_out=None, u=None, write_f: int = 0, g=None,
               tail: int = 0, tail_out=None, tail_stride: int = 0, cref=None,
               cref_stride: int = 0, cref_e=None, cref_e_stride: int = 0, partials=None,
-              stats_depth=None, stats_res=None, stream=None) -> None:
+              stats_depth=None, stats_res=None, z_out=None, z_stride: int = 0,
+              stream=None) -> None:
         t = self._torch
         nI, n = int(n_intervals), self.prog.n_x
         if nI <= 0:
@@ -275,6 +278,8 @@ class CallablePlan:
             if tail == 1:
                 self._rows(tail_out, nI, tail_stride).copy_(z)
             else:
+                if z_out is not None:
+                    self._rows(z_out, nI, z_stride).copy_(z)
                 cr = self._rows(cref, nI, cref_stride)
                 if cref_e is not None:
                     cr = cr + self._rows(cref_e, nI, cref_e_stride)

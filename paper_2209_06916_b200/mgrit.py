@@ -29,6 +29,14 @@ one C-step (residual step) per interval instead of m steps.  Bitwise the same
 iterate and history (``ELIDE_OPENING_F_RELAX = False`` runs the full pass;
 tests/test_gpu_parity.py compares both).
 
+Closing residual step = next opening C-relaxation (fine level, nu >= 1): the
+fused norm of the CF pass evaluates r_{k+1} = (g + Phi u_{km+m-1}) - u_{(k+1)m}; its
+first term is exactly the value c_relax (mgrit.py:148-149) computes at the start of
+the next cycle from the same stored F-point.  The CF pass stores it (``z_out`` of
+``mgb_relax_args``) and the next cycle starts from it: iterations >= 2 run the
+fine level in exactly two sweeps (FR and CF).  ``REUSE_CLOSING_STEP = False``
+recomputes it.
+
 First interval of a coarse level (nu >= 1): the error at t = 0 is zero, so on
 levels >= 1 interval 0 starts from the same zero C-point in the FC, FR and CF
 passes of a cycle (mgrit.py:231-247): the FR pass recomputes the FC pass's
@@ -60,6 +68,11 @@ POISON_SKIPPED_ROWS = False
 #: iterations >= 2 of ``solve`` read the F-points the previous closing F-relaxation left
 #: instead of recomputing them (module docstring); False: recompute like the reference
 ELIDE_OPENING_F_RELAX = True
+#: fine level: the residual step that closes a cycle (the fused norm of the CF pass) computes
+#: g + Phi u_{km+m-1}, which IS the C-relaxation the next cycle opens with: the CF pass stores
+#: it and the next cycle skips its first FC pass altogether (module docstring); False: the
+#: next cycle recomputes it with one C-step per interval
+REUSE_CLOSING_STEP = True
 #: coarse levels: the first interval starts from e_0 = 0 in every pass, so its FR and CF
 #: work repeats the FC pass bit for bit (module docstring); False: recompute
 ELIDE_FIRST_INTERVAL = True
@@ -276,6 +289,9 @@ class MgritSolver:
         self.profile = None
         #: plan tag: solvers that run concurrently (solve_many) get private plans
         self.plan_tag = None
+        #: REUSE_CLOSING_STEP needs per-cycle buffer swaps (not for CUDA-graph replays)
+        self._use_z = True
+        self._z_valid = False
 
     # ---------------------------------------------------------- buffers
     def _build(self):
@@ -358,7 +374,12 @@ class MgritSolver:
         k0 = 1 if skip0 else 0
         for i in range(cfg.nu):
             dst = L.cbuf[i % 2]
-            if i == 0 and f_relaxed:  # C-step from the stored last F-point of every interval
+            if i == 0 and f_relaxed and l == 0 and self._z_valid:
+                # the previous cycle's closing residual step left these C-relaxed values
+                L.cbuf[0], L.zbuf = L.zbuf, L.cbuf[0]
+                dst = L.cbuf[0]
+                self._z_valid = False
+            elif i == 0 and f_relaxed:  # C-step from the stored last F-point of every interval
                 self._timed(f"L{l}.FC", plan.relax, nI, m, 0, c_src=u + (m - 1) * row,
                             c_stride=m * n, tail=1, tail_out=ptr(dst) + row, tail_stride=n, g=g)
             elif i == 0 and skip0 and u_zero:  # interval 0's F-points are final: written here
@@ -413,13 +434,20 @@ class MgritSolver:
                 torch = self._torch
                 torch.add(L.cbuf[(cfg.nu - 1) % 2][1], uC[1], out=self.ucoarse[l][m])
         else:
+            zkw = {}
+            if (l == 0 and fuse_norm and self._use_z and REUSE_CLOSING_STEP and ELIDE_OPENING_F_RELAX
+                    and plan.prog.kind in ("stencil", "rk", "callable")):
+                if getattr(L, "zbuf", None) is None:
+                    L.zbuf = self._torch.empty_like(L.cbuf[0])
+                zkw = dict(z_out=ptr(L.zbuf) + row, z_stride=n)
+                self._z_valid = True
             self._timed(f"L{l}.CF", plan.relax, nI, m, m - 1, c_src=c_src, c_stride=c_stride,
                         c_src0=u0row, e=ptr(uC),
                         e_stride=n, c_out=u, c_out_stride=m * n, c_last_out=u + nI * m * row,
                         u=u, write_f=2, g=g,
                         tail=2 if fuse_norm else 0, cref=(c_src + row) if fuse_norm else None,
                         cref_stride=n, cref_e=ptr(uC) + row, cref_e_stride=n,
-                        partials=ptr(self.partials) if fuse_norm else None)
+                        partials=ptr(self.partials) if fuse_norm else None, **zkw)
         if want_norm and not fuse_norm:
             self._timed("L0.R", self._residual_partials, u, g)
 
@@ -489,6 +517,7 @@ class MgritSolver:
             u = self.initial_state()
         ud, uh, pending = self._upload(u, split=True)
         up = ptr(ud)
+        self._z_valid = False
         hook = None
         if pending is None:
             torch.cuda.synchronize()
@@ -646,6 +675,7 @@ def solve_many(jobs, streams: Optional[int] = 8, graphs: bool = True,
         d = st[k]
         sol = MgritSolver(d["problem"], d["config"])
         sol.plan_tag = ("slot", slot)
+        sol._use_z = False  # graph replays use fixed buffers
         d.update(sol=sol, slot=slot, stream=pool[slot])
         with torch.cuda.stream(pool[slot]):
             sol._build()

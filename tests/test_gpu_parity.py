@@ -495,6 +495,7 @@ def test_elided_opening_f_relaxation_is_bitwise_the_full_pass(fam, p, c, n_x, n_
     rep_a = P.solve(prob, cfg, initial_iterate=u_a)
     monkeypatch.setattr(M, "ELIDE_OPENING_F_RELAX", False)
     monkeypatch.setattr(M, "ELIDE_FIRST_INTERVAL", False)
+    monkeypatch.setattr(M, "REUSE_CLOSING_STEP", False)
     rep_b = P.solve(prob, cfg, initial_iterate=u_b)
     assert rep_a.iterations == rep_b.iterations >= 2
     if fam == "erk" and cyc != "two_level" and n_x >= 1024:

@@ -70,6 +70,7 @@ for fam, p, c, n_x, n_t, m, cyc, nu in %r:
     row = {}
     for name, flags in (("elided", (True, True)), ("full", (False, False))):
         M.ELIDE_OPENING_F_RELAX, M.ELIDE_FIRST_INTERVAL = flags
+        M.REUSE_CLOSING_STEP = flags[0]
         u = u0.copy()
         rep = P.solve(prob, cfg, initial_iterate=u)
         row[name] = [rep.residual_norms, hashlib.sha256(u.tobytes()).hexdigest()]

@@ -11,7 +11,7 @@ cfg = P.MgritConfig(cycle=cyc, nu=nu, max_iters=6)
 u0 = P.MgritSolver(prob, cfg).initial_state()
 res = {}
 for name, (a, b) in {"both": (True, True), "open_only": (True, False), "first_only": (False, True), "none": (False, False)}.items():
-    M.ELIDE_OPENING_F_RELAX, M.ELIDE_FIRST_INTERVAL = a, b
+    M.ELIDE_OPENING_F_RELAX, M.ELIDE_FIRST_INTERVAL, M.REUSE_CLOSING_STEP = a, b, a
     u = u0.copy()
     rep = P.solve(prob, cfg, initial_iterate=u)
     res[name] = (np.array(rep.residual_norms), u)
