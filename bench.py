@@ -164,7 +164,8 @@ def pass_work(cf, level, n_int, m, prog, kind, steps=None):
       FR: m steps: reads the C-point row and the reference C-point row, writes
           the residual row;
       CF: m steps (m-1 F + the residual tail): reads the C-point and correction
-          rows once, writes every F/C row once (fine level: the iterate).
+          rows once, writes every F/C row once (fine level: the iterate; the
+          C-relaxed row it also stores for the next cycle is not counted).
     flops = 2 * taps per point-step (one multiply + one add per tap)."""
     n, taps = cf.n_x, len(prog.offsets)
     if prog.kind == "rk":
